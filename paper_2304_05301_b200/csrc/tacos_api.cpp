@@ -1,0 +1,1147 @@
+// tacos_api.cpp -- host runtime behind include/tacos.h (C ABI).
+//
+// Validation, cost quantization (a1), CSR construction,
+// strong connectivity, plan / device memory management (a caching device and
+// pinned-host allocator), orchestration of the kernels in tacos_kernels.cu
+// (a2-a8), and the host verifier behind tacos_eval.
+// Product side only: nothing here is shared with the CPU oracle (oracle/).
+#include "tacos.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "tacos_internal.h"
+
+using namespace tacos;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) return fail(TACOS_E_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// caching allocators (device and pinned host): freed blocks are kept per
+// (device, size class) and reused, so repeated synthesize calls do not pay
+// cudaMalloc / cudaMallocHost.
+// ---------------------------------------------------------------------------
+namespace {
+size_t size_class(size_t n) {
+  if (n <= 4096) return 4096;
+  if (n <= (2u << 20)) {
+    size_t c = 4096;
+    while (c < n) c <<= 1;
+    return c;
+  }
+  return (n + (2u << 20) - 1) / (2u << 20) * (2u << 20);
+}
+
+struct Pool {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void *> free_blocks;
+  bool pinned;
+  explicit Pool(bool pinned_) : pinned(pinned_) {}
+  void *alloc(int dev, size_t n, size_t *cls_out) {
+    const size_t cls = size_class(n);
+    *cls_out = cls;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free_blocks.find({dev, cls});
+      if (it != free_blocks.end()) {
+        void *p = it->second;
+        free_blocks.erase(it);
+        return p;
+      }
+    }
+    void *p = nullptr;
+    cudaError_t e = pinned ? cudaMallocHost(&p, cls) : cudaMalloc(&p, cls);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      // trim the cache and retry once
+      std::vector<std::pair<int, void *>> drop;
+      {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto &kv : free_blocks) drop.push_back({kv.first.first, kv.second});
+        free_blocks.clear();
+      }
+      for (auto &d : drop) {
+        if (pinned) cudaFreeHost(d.second);
+        else cudaFree(d.second);
+      }
+      e = pinned ? cudaMallocHost(&p, cls) : cudaMalloc(&p, cls);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+    }
+    return p;
+  }
+  void release(int dev, void *p, size_t cls) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(mu);
+    free_blocks.insert({{dev, cls}, p});
+  }
+};
+
+Pool &device_pool() {
+  static Pool *p = new Pool(false);  // intentionally leaked: lives until process exit
+  return *p;
+}
+Pool &pinned_pool() {
+  static Pool *p = new Pool(true);
+  return *p;
+}
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t cls = 0;
+  int dev = -1;
+};
+
+int cuda_device_ok(int *dev_out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(TACOS_E_CUDA, "no CUDA device available (%s)", e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+  }
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  *dev_out = dev;
+  return TACOS_OK;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// topology
+// ---------------------------------------------------------------------------
+struct tacos_topology {
+  int32_t N = 0, L = 0;
+  std::vector<int32_t> src, dst;
+  std::vector<uint32_t> alpha, bw;
+  std::vector<int32_t> rev;  // link dst->src or -1
+  bool strongly_connected = false;
+  // orientation 0 = G (grouped by dst), 1 = G^T (grouped by src)
+  std::vector<uint32_t> in_ptr[2], pos_lid[2], pos_src[2], pos_dst[2];
+  int device = -1;
+  uint32_t *d_in_ptr[2] = {nullptr, nullptr}, *d_pos_lid[2] = {nullptr, nullptr};
+  uint32_t *d_pos_src[2] = {nullptr, nullptr}, *d_pos_dst[2] = {nullptr, nullptr};
+  uint32_t *d_src = nullptr, *d_dst = nullptr;
+  int32_t *d_rev = nullptr;
+  std::vector<DevBuf> bufs;
+  ~tacos_topology() {
+    for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
+  }
+};
+
+namespace {
+template <typename T>
+int upload(std::vector<DevBuf> &bufs, int dev, const T *h, size_t n, T **d_out, cudaStream_t st = nullptr) {
+  DevBuf b;
+  b.dev = dev;
+  b.p = device_pool().alloc(dev, n * sizeof(T) + 16, &b.cls);
+  if (!b.p) return fail(TACOS_E_NOMEM, "device allocation of %zu bytes failed", n * sizeof(T));
+  bufs.push_back(b);
+  if (n) CUDA_TRY(cudaMemcpyAsync(b.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+  *d_out = reinterpret_cast<T *>(b.p);
+  return TACOS_OK;
+}
+
+int dev_alloc(std::vector<DevBuf> &bufs, int dev, size_t n, void **d_out) {
+  DevBuf b;
+  b.dev = dev;
+  b.p = device_pool().alloc(dev, n + 16, &b.cls);
+  if (!b.p) return fail(TACOS_E_NOMEM, "device allocation of %zu bytes failed", n);
+  bufs.push_back(b);
+  *d_out = b.p;
+  return TACOS_OK;
+}
+
+bool reach_all(int32_t N, const std::vector<uint32_t> &ptr, const std::vector<uint32_t> &pos_src) {
+  // BFS from 0 following reversed CSR edges (in-links): reaches every node that can reach 0
+  std::vector<char> seen(N, 0);
+  std::vector<int32_t> stack{0};
+  seen[0] = 1;
+  int32_t cnt = 1;
+  while (!stack.empty()) {
+    int32_t v = stack.back();
+    stack.pop_back();
+    for (uint32_t p = ptr[v]; p < ptr[v + 1]; ++p) {
+      int32_t u = (int32_t)pos_src[p];
+      if (!seen[u]) {
+        seen[u] = 1;
+        ++cnt;
+        stack.push_back(u);
+      }
+    }
+  }
+  return cnt == N;
+}
+
+// a1: w = ceil((alpha*bw + n) / (bw*f)) exactly (P:L104 alpha + n/bw; P:L172 ceil(l/f))
+int quantize(uint32_t alpha, uint32_t bw, uint64_t n, uint32_t f, uint32_t *w_out) {
+  if (bw == 0) return TACOS_E_TOPOLOGY;
+  const unsigned __int128 num = (unsigned __int128)alpha * bw + n;
+  const unsigned __int128 den = (unsigned __int128)bw * (f ? f : 1u);
+  const unsigned __int128 q = num / den + (num % den != 0 ? 1 : 0);
+  if (q == 0) return TACOS_E_TOPOLOGY;
+  if (q > 0xFFFFFFFFull) return TACOS_E_OVERFLOW;
+  *w_out = (uint32_t)q;
+  return TACOS_OK;
+}
+
+int link_costs(const tacos_topology *t, uint64_t n, uint32_t f, std::vector<uint32_t> &w) {
+  w.resize(t->L);
+  for (int32_t l = 0; l < t->L; ++l) {
+    int rc = quantize(t->alpha[l], t->bw[l], n, f, &w[l]);
+    if (rc == TACOS_E_TOPOLOGY) return fail(rc, "link %d has zero cost (alpha = n = 0)", l);
+    if (rc == TACOS_E_OVERFLOW) return fail(rc, "link %d cost exceeds 2^32 time units", l);
+    if (rc) return fail(rc, "link %d: bad cost", l);
+  }
+  return TACOS_OK;
+}
+
+bool symmetric_for(const tacos_topology *t, const std::vector<uint32_t> &w) {
+  for (int32_t l = 0; l < t->L; ++l) {
+    if (t->rev[l] < 0 || w[t->rev[l]] != w[l]) return false;
+  }
+  return true;
+}
+}  // namespace
+
+extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst,
+                                   const uint32_t *alpha_ns, const uint32_t *bw, tacos_topology **out) {
+  if (out) *out = nullptr;
+  if (!out || !src || !dst || !alpha_ns || !bw) return fail(TACOS_E_INVALID_ARG, "null argument");
+  if (n_npus < 2) return fail(TACOS_E_INVALID_ARG, "n_npus = %d < 2", n_npus);
+  if (n_links < 1 || n_links >= (1 << 24)) return fail(TACOS_E_INVALID_ARG, "n_links = %d out of [1, 2^24)", n_links);
+  std::unique_ptr<tacos_topology> t(new (std::nothrow) tacos_topology());
+  if (!t) return fail(TACOS_E_NOMEM, "host allocation failed");
+  t->N = n_npus;
+  t->L = n_links;
+  t->src.assign(src, src + n_links);
+  t->dst.assign(dst, dst + n_links);
+  t->alpha.assign(alpha_ns, alpha_ns + n_links);
+  t->bw.assign(bw, bw + n_links);
+  std::unordered_map<uint64_t, int32_t> pair_id;
+  pair_id.reserve((size_t)n_links * 2);
+  for (int32_t l = 0; l < n_links; ++l) {
+    const int32_t a = src[l], b = dst[l];
+    if (a < 0 || a >= n_npus || b < 0 || b >= n_npus)
+      return fail(TACOS_E_TOPOLOGY, "link %d: endpoint out of range (%d -> %d)", l, a, b);
+    if (a == b) return fail(TACOS_E_TOPOLOGY, "link %d: self-loop on NPU %d", l, a);
+    if (bw[l] == 0) return fail(TACOS_E_TOPOLOGY, "link %d: bandwidth 0", l);
+    const uint64_t key = ((uint64_t)(uint32_t)a << 32) | (uint32_t)b;
+    if (!pair_id.emplace(key, l).second)
+      return fail(TACOS_E_TOPOLOGY, "link %d duplicates link %d (%d -> %d)", l, pair_id[key], a, b);
+  }
+  t->rev.assign(n_links, -1);
+  for (int32_t l = 0; l < n_links; ++l) {
+    auto it = pair_id.find(((uint64_t)(uint32_t)dst[l] << 32) | (uint32_t)src[l]);
+    if (it != pair_id.end()) t->rev[l] = it->second;
+  }
+  // CSR per orientation; within a destination, positions in ascending link id
+  for (int o = 0; o < 2; ++o) {
+    const int32_t *key = o == 0 ? dst : src;
+    const int32_t *oth = o == 0 ? src : dst;
+    auto &ptr = t->in_ptr[o];
+    ptr.assign(n_npus + 1, 0);
+    for (int32_t l = 0; l < n_links; ++l) ptr[key[l] + 1]++;
+    for (int32_t d = 0; d < n_npus; ++d) ptr[d + 1] += ptr[d];
+    std::vector<uint32_t> fill(ptr.begin(), ptr.end() - 1);
+    t->pos_lid[o].resize(n_links);
+    t->pos_src[o].resize(n_links);
+    t->pos_dst[o].resize(n_links);
+    for (int32_t l = 0; l < n_links; ++l) {
+      const uint32_t p = fill[key[l]]++;
+      t->pos_lid[o][p] = (uint32_t)l;
+      t->pos_src[o][p] = (uint32_t)oth[l];
+      t->pos_dst[o][p] = (uint32_t)key[l];
+    }
+  }
+  t->strongly_connected = reach_all(n_npus, t->in_ptr[0], t->pos_src[0]) && reach_all(n_npus, t->in_ptr[1], t->pos_src[1]);
+
+  int dev = -1;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) {
+    t->device = dev;
+    int rc;
+    for (int o = 0; o < 2; ++o) {
+      if ((rc = upload(t->bufs, dev, t->in_ptr[o].data(), t->in_ptr[o].size(), &t->d_in_ptr[o]))) return rc;
+      if ((rc = upload(t->bufs, dev, t->pos_lid[o].data(), (size_t)n_links, &t->d_pos_lid[o]))) return rc;
+      if ((rc = upload(t->bufs, dev, t->pos_src[o].data(), (size_t)n_links, &t->d_pos_src[o]))) return rc;
+      if ((rc = upload(t->bufs, dev, t->pos_dst[o].data(), (size_t)n_links, &t->d_pos_dst[o]))) return rc;
+    }
+    std::vector<uint32_t> us(src, src + n_links), ud(dst, dst + n_links);
+    if ((rc = upload(t->bufs, dev, us.data(), (size_t)n_links, &t->d_src))) return rc;
+    if ((rc = upload(t->bufs, dev, ud.data(), (size_t)n_links, &t->d_dst))) return rc;
+    if ((rc = upload(t->bufs, dev, t->rev.data(), (size_t)n_links, &t->d_rev))) return rc;
+    CUDA_TRY(cudaStreamSynchronize(nullptr));
+  } else {
+    cudaGetLastError();
+  }
+  *out = t.release();
+  return TACOS_OK;
+}
+
+extern "C" void tacos_free_topology(tacos_topology *t) { delete t; }
+extern "C" int32_t tacos_topology_num_npus(const tacos_topology *t) { return t ? t->N : -1; }
+extern "C" int32_t tacos_topology_num_links(const tacos_topology *t) { return t ? t->L : -1; }
+extern "C" int tacos_topology_strongly_connected(const tacos_topology *t) { return t && t->strongly_connected ? 1 : 0; }
+
+extern "C" int tacos_link_costs(const tacos_topology *t, uint64_t chunk_bytes, uint32_t f, uint32_t *w_out) {
+  if (!t || !w_out) return fail(TACOS_E_INVALID_ARG, "null argument");
+  std::vector<uint32_t> w;
+  int rc = link_costs(t, chunk_bytes, f ? f : 1u, w);
+  if (rc) return rc;
+  std::memcpy(w_out, w.data(), w.size() * 4);
+  return TACOS_OK;
+}
+
+extern "C" int tacos_is_symmetric(const tacos_topology *t, uint64_t chunk_bytes, uint32_t f) {
+  if (!t) return 0;
+  std::vector<uint32_t> w;
+  if (link_costs(t, chunk_bytes, f ? f : 1u, w)) return 0;
+  return symmetric_for(t, w) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// plan: device state for a batch of topologies sharing the params
+// ---------------------------------------------------------------------------
+namespace {
+struct Part {
+  const tacos_topology *topo = nullptr;
+  uint32_t N = 0, L = 0, C = 0, k = 0, Wp = 0, P = 0, VPL = 0;
+  bool custom = false, symmetric = false, rs_search = false;
+  uint64_t required = 0;
+  std::vector<uint32_t> w;
+  DevTopo htopo[2];
+  DevTopo *d_topo[2] = {nullptr, nullptr};
+  uint32_t *d_w = nullptr;
+  uint32_t job_base = 0, n_jobs = 0;  // jobs [job_base, job_base + n_jobs): S (sigma 0) then S (sigma 1)
+  Rec *d_rec = nullptr;               // n_jobs * required records
+  uint64_t *d_keys = nullptr;         // 2
+  uint64_t *d_stats = nullptr;        // 5
+  uint64_t *d_times_ag = nullptr, *d_times_rs = nullptr;
+};
+struct Group {
+  uint32_t P, VPL;
+  Layout lay;
+  uint32_t job_begin, job_end;
+};
+}  // namespace
+
+struct tacos_plan {
+  int device = -1;
+  tacos_synth_params p{};
+  std::vector<uint32_t> pre, post;  // CUSTOM copies (unpadded rows)
+  std::vector<Part> parts;
+  std::vector<Group> groups;
+  std::vector<Job> jobs;
+  Job *d_jobs = nullptr;
+  JobOut *d_outs = nullptr;
+  unsigned char *d_rows = nullptr, *d_links = nullptr;
+  void *d_sort = nullptr;
+  size_t sort_bytes = 0;
+  uint64_t *h_small = nullptr;  // pinned: per part {keys[2], stats[5]}
+  DevBuf h_small_buf;
+  std::vector<DevBuf> bufs;
+  uint32_t last_launches = 0;
+  ~tacos_plan() {
+    for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
+    if (h_small_buf.p) pinned_pool().release(h_small_buf.dev, h_small_buf.p, h_small_buf.cls);
+  }
+};
+
+namespace {
+int validate_params(const tacos_synth_params *p) {
+  if (!p) return fail(TACOS_E_INVALID_ARG, "null params");
+  if (p->collective < TACOS_ALL_GATHER || p->collective > TACOS_CUSTOM)
+    return fail(TACOS_E_INVALID_ARG, "bad collective %d", p->collective);
+  if (p->chunk_bytes == 0) return fail(TACOS_E_INVALID_ARG, "chunk_bytes = 0");
+  if (p->n_seeds < 1) return fail(TACOS_E_INVALID_ARG, "n_seeds = 0");
+  if ((uint64_t)p->seed_offset + p->n_seeds > (1ull << kKeySeedBits))
+    return fail(TACOS_E_OVERFLOW, "seed index beyond 2^%d", kKeySeedBits);
+  if (p->collective == TACOS_CUSTOM) {
+    if (!p->pre_bits || !p->post_bits || p->n_chunks < 1) return fail(TACOS_E_INVALID_ARG, "CUSTOM needs pre/post/n_chunks");
+  } else if (p->chunks_per_npu < 1) {
+    return fail(TACOS_E_INVALID_ARG, "chunks_per_npu = 0");
+  }
+  return TACOS_OK;
+}
+
+uint32_t pow2_at_least(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p, tacos_plan **out) {
+  *out = nullptr;
+  int rc = validate_params(p);
+  if (rc) return rc;
+  int dev = -1;
+  if ((rc = cuda_device_ok(&dev))) return rc;
+  std::unique_ptr<tacos_plan> pl(new (std::nothrow) tacos_plan());
+  if (!pl) return fail(TACOS_E_NOMEM, "host allocation failed");
+  pl->device = dev;
+  pl->p = *p;
+  if (pl->p.time_unit_ns == 0) pl->p.time_unit_ns = 1;
+  const uint32_t S = p->n_seeds;
+  const bool custom = p->collective == TACOS_CUSTOM;
+  const bool need_rs = p->collective == TACOS_REDUCE_SCATTER || p->collective == TACOS_ALL_REDUCE;
+  const bool record = (p->flags & TACOS_FLAG_NO_SCHEDULE) == 0;
+
+  // ---- per-topology host preparation ----
+  pl->parts.resize(n_topos);
+  uint32_t n_jobs = 0;
+  for (uint32_t i = 0; i < n_topos; ++i) {
+    const tacos_topology *t = topos[i];
+    if (!t) return fail(TACOS_E_INVALID_ARG, "null topology %u", i);
+    if (t->device != dev) return fail(TACOS_E_CUDA, "topology %u was loaded on device %d, current device %d", i, t->device, dev);
+    Part &pt = pl->parts[i];
+    pt.topo = t;
+    pt.N = (uint32_t)t->N;
+    pt.L = (uint32_t)t->L;
+    pt.custom = custom;
+    if (custom) {
+      pt.C = p->n_chunks;
+      pt.k = 0;
+    } else {
+      const uint64_t C = (uint64_t)pt.N * p->chunks_per_npu;
+      if (C > kMaxChunks) return fail(TACOS_E_OVERFLOW, "C = %llu chunks exceeds %u", (unsigned long long)C, kMaxChunks);
+      pt.C = (uint32_t)C;
+      pt.k = p->chunks_per_npu;
+      if (!t->strongly_connected)
+        return fail(TACOS_E_UNREACHABLE, "topology %u is not strongly connected", i);
+    }
+    if (pt.C > kMaxChunks) return fail(TACOS_E_OVERFLOW, "C = %u chunks exceeds %u", pt.C, kMaxChunks);
+    if ((rc = link_costs(t, p->chunk_bytes, pl->p.time_unit_ns, pt.w))) return rc;
+    pt.symmetric = symmetric_for(t, pt.w);
+    pt.rs_search = need_rs && !pt.symmetric;
+    const uint32_t W0 = (pt.C + 31u) / 32u;
+    const uint32_t vec = (W0 + 3u) / 4u;
+    pt.P = std::min<uint32_t>(32u, pow2_at_least(vec));
+    pt.VPL = (vec + pt.P - 1u) / pt.P;
+    if (pt.VPL == 3) pt.VPL = 4;
+    if (pt.VPL > (uint32_t)kMaxVPL) return fail(TACOS_E_OVERFLOW, "C too large");
+    pt.Wp = 4u * pt.P * pt.VPL;
+    if (custom) {
+      if (n_topos != 1) return fail(TACOS_E_INVALID_ARG, "CUSTOM collectives are not batched over topologies");
+      const size_t words = (size_t)pt.N * W0;
+      pl->pre.assign(p->pre_bits, p->pre_bits + words);
+      pl->post.assign(p->post_bits, p->post_bits + words);
+      uint64_t req = 0;
+      for (size_t q = 0; q < words; ++q) {
+        if (pl->pre[q] & ~pl->post[q]) return fail(TACOS_E_INVALID_ARG, "pre is not a subset of post (row %zu)", q / W0);
+        const uint32_t valid = (q % W0 == W0 - 1 && (pt.C & 31u)) ? ((1u << (pt.C & 31u)) - 1u) : 0xFFFFFFFFu;
+        if ((pl->pre[q] | pl->post[q]) & ~valid) return fail(TACOS_E_INVALID_ARG, "bits beyond C set");
+        req += (uint64_t)__builtin_popcount(pl->post[q] & ~pl->pre[q]);
+      }
+      pt.required = req;
+    } else {
+      pt.required = (uint64_t)pt.C * (pt.N - 1u);
+    }
+    pt.job_base = n_jobs;
+    pt.n_jobs = S * (pt.rs_search ? 2u : 1u);
+    n_jobs += pt.n_jobs;
+  }
+
+  // ---- groups by row shape: one launch each, max layout over members ----
+  std::vector<uint32_t> order(n_topos);
+  for (uint32_t i = 0; i < n_topos; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return std::make_pair(pl->parts[a].P, pl->parts[a].VPL) < std::make_pair(pl->parts[b].P, pl->parts[b].VPL);
+  });
+  int smem_optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t smem_limit = (size_t)smem_optin > 1024 ? (size_t)smem_optin - 1024 : 0;
+  // re-number jobs in group order
+  n_jobs = 0;
+  for (size_t gi = 0; gi < order.size();) {
+    const uint32_t P0 = pl->parts[order[gi]].P, V0 = pl->parts[order[gi]].VPL;
+    uint32_t maxN = 0, maxL = 0, maxW = 0;
+    size_t gj = gi;
+    const uint32_t begin = n_jobs;
+    while (gj < order.size() && pl->parts[order[gj]].P == P0 && pl->parts[order[gj]].VPL == V0) {
+      Part &pt = pl->parts[order[gj]];
+      maxN = std::max(maxN, pt.N);
+      maxL = std::max(maxL, pt.L);
+      maxW = std::max(maxW, pt.Wp);
+      pt.job_base = n_jobs;
+      n_jobs += pt.n_jobs;
+      ++gj;
+    }
+    Group g;
+    g.P = P0;
+    g.VPL = V0;
+    g.lay = make_layout(maxN, maxL, maxW, P0, V0, smem_limit);
+    g.job_begin = begin;
+    g.job_end = n_jobs;
+    pl->groups.push_back(g);
+    gi = gj;
+  }
+
+  // ---- device allocations ----
+  auto &bufs = pl->bufs;
+  void *vp = nullptr;
+  size_t rows_total = 0, links_total = 0;
+  for (auto &g : pl->groups) {
+    const size_t nj = g.job_end - g.job_begin;
+    if (!g.lay.rows_in_smem) rows_total += nj * g.lay.rows_bytes;
+    if (!g.lay.links_in_smem) links_total += nj * g.lay.links_bytes;
+  }
+  if (rows_total) {
+    if ((rc = dev_alloc(bufs, dev, rows_total, &vp))) return rc;
+    pl->d_rows = reinterpret_cast<unsigned char *>(vp);
+  }
+  if (links_total) {
+    if ((rc = dev_alloc(bufs, dev, links_total, &vp))) return rc;
+    pl->d_links = reinterpret_cast<unsigned char *>(vp);
+  }
+  if ((rc = dev_alloc(bufs, dev, sizeof(JobOut) * n_jobs, &vp))) return rc;
+  pl->d_outs = reinterpret_cast<JobOut *>(vp);
+  uint64_t max_M = 0;
+  for (uint32_t i = 0; i < n_topos; ++i) {
+    Part &pt = pl->parts[i];
+    const tacos_topology *t = pt.topo;
+    if ((rc = upload(bufs, dev, pt.w.data(), pt.w.size(), &pt.d_w))) return rc;
+    // per-position costs for both orientations
+    uint32_t *d_pos_w[2];
+    for (int o = 0; o < 2; ++o) {
+      std::vector<uint32_t> pw(pt.L);
+      for (uint32_t q = 0; q < pt.L; ++q) pw[q] = pt.w[t->pos_lid[o][q]];
+      if ((rc = upload(bufs, dev, pw.data(), pw.size(), &d_pos_w[o]))) return rc;
+    }
+    uint32_t *d_pre = nullptr, *d_post = nullptr;
+    if (custom) {
+      const uint32_t W0 = (pt.C + 31u) / 32u;
+      std::vector<uint32_t> pre_p((size_t)pt.N * pt.Wp, 0u), post_p((size_t)pt.N * pt.Wp, 0u);
+      for (uint32_t x = 0; x < pt.N; ++x)
+        for (uint32_t q = 0; q < W0; ++q) {
+          pre_p[(size_t)x * pt.Wp + q] = pl->pre[(size_t)x * W0 + q];
+          post_p[(size_t)x * pt.Wp + q] = pl->post[(size_t)x * W0 + q];
+        }
+      if ((rc = upload(bufs, dev, pre_p.data(), pre_p.size(), &d_pre))) return rc;
+      if ((rc = upload(bufs, dev, post_p.data(), post_p.size(), &d_post))) return rc;
+    }
+    for (int o = 0; o < 2; ++o) {
+      DevTopo &h = pt.htopo[o];
+      h.N = pt.N;
+      h.L = pt.L;
+      h.C = pt.C;
+      h.k = pt.k;
+      h.Wp = pt.Wp;
+      h.P = pt.P;
+      h.VPL = pt.VPL;
+      h.custom = custom ? 1u : 0u;
+      h.required = pt.required;
+      h.in_ptr = t->d_in_ptr[o];
+      h.p_src = t->d_pos_src[o];
+      h.p_dst = t->d_pos_dst[o];
+      h.p_w = d_pos_w[o];
+      h.p_lid = t->d_pos_lid[o];
+      h.pre = d_pre;
+      h.post = d_post;
+      if ((rc = upload(bufs, dev, &h, 1, &pt.d_topo[o]))) return rc;
+    }
+    if (record) {
+      if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.required * pt.n_jobs, &vp))) return rc;
+      pt.d_rec = reinterpret_cast<Rec *>(vp);
+    }
+    if ((rc = dev_alloc(bufs, dev, 8 * 7, &vp))) return rc;
+    pt.d_keys = reinterpret_cast<uint64_t *>(vp);
+    pt.d_stats = pt.d_keys + 2;
+    if ((rc = dev_alloc(bufs, dev, 8 * (size_t)S, &vp))) return rc;
+    pt.d_times_ag = reinterpret_cast<uint64_t *>(vp);
+    if (pt.rs_search) {
+      if ((rc = dev_alloc(bufs, dev, 8 * (size_t)S, &vp))) return rc;
+      pt.d_times_rs = reinterpret_cast<uint64_t *>(vp);
+    }
+    if (need_rs && record) max_M = std::max(max_M, pt.required);
+  }
+  if (max_M) {
+    pl->sort_bytes = rs_sort_scratch_bytes(max_M);
+    if ((rc = dev_alloc(bufs, dev, pl->sort_bytes, &pl->d_sort))) return rc;
+  }
+  // ---- job table ----
+  pl->jobs.resize(n_jobs);
+  size_t rows_off = 0, links_off = 0;
+  for (auto &g : pl->groups) {
+    for (uint32_t i = 0; i < n_topos; ++i) {
+      Part &pt = pl->parts[i];
+      if (pt.job_base < g.job_begin || pt.job_base >= g.job_end) continue;
+      for (uint32_t j = 0; j < pt.n_jobs; ++j) {
+        const uint32_t sigma = j >= S ? 1u : 0u;
+        const uint32_t si = j % S;
+        Job &jb = pl->jobs[pt.job_base + j];
+        jb.topo = pt.d_topo[sigma];
+        jb.seed = p->base_seed + p->seed_offset + si;
+        jb.sigma = sigma;
+        jb.out_slot = pt.job_base + j;
+        jb.rec = record ? pt.d_rec + (size_t)j * pt.required : nullptr;
+        jb.g_rows = nullptr;
+        jb.g_links = nullptr;
+        if (!g.lay.rows_in_smem) {
+          jb.g_rows = reinterpret_cast<uint32_t *>(pl->d_rows + rows_off);
+          rows_off += g.lay.rows_bytes;
+        }
+        if (!g.lay.links_in_smem) {
+          jb.g_links = pl->d_links + links_off;
+          links_off += g.lay.links_bytes;
+        }
+      }
+    }
+  }
+  if ((rc = upload(bufs, dev, pl->jobs.data(), pl->jobs.size(), &pl->d_jobs))) return rc;
+  pl->h_small_buf.dev = dev;
+  pl->h_small_buf.p = pinned_pool().alloc(dev, 8 * 8 * (size_t)n_topos, &pl->h_small_buf.cls);
+  if (!pl->h_small_buf.p) return fail(TACOS_E_NOMEM, "pinned allocation failed");
+  pl->h_small = reinterpret_cast<uint64_t *>(pl->h_small_buf.p);
+  CUDA_TRY(cudaStreamSynchronize(nullptr));
+  *out = pl.release();
+  return TACOS_OK;
+}
+
+int plan_search(tacos_plan *pl, cudaStream_t st) {
+  int rc;
+  pl->last_launches = 0;
+  for (auto &g : pl->groups) {
+    if ((rc = launch_greedy(g.lay, g.P, g.VPL, pl->d_jobs + g.job_begin, g.job_end - g.job_begin, pl->d_outs, st)))
+      return fail(rc, "%s", cuda_error_string());
+    pl->last_launches++;
+  }
+  const uint32_t S = pl->p.n_seeds;
+  for (auto &pt : pl->parts) {
+    if ((rc = launch_best_keys(pl->d_outs + pt.job_base, S, pl->p.seed_offset, S, pt.rs_search ? 1u : 0u, pt.d_keys,
+                               pt.d_stats, pt.d_times_ag, pt.d_times_rs, st)))
+      return fail(rc, "%s", cuda_error_string());
+    pl->last_launches++;
+  }
+  return TACOS_OK;
+}
+
+// Read keys + stats of every part (one D2H, one sync).
+int plan_read_small(tacos_plan *pl, cudaStream_t st) {
+  for (size_t i = 0; i < pl->parts.size(); ++i)
+    CUDA_TRY(cudaMemcpyAsync(pl->h_small + 8 * i, pl->parts[i].d_keys, 7 * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TACOS_OK;
+}
+
+uint64_t sends_per_result(const tacos_plan *pl, const Part &pt) {
+  if (pl->p.flags & TACOS_FLAG_NO_SCHEDULE) return 0;
+  return pl->p.collective == TACOS_ALL_REDUCE ? 2 * pt.required : pt.required;
+}
+
+// Emit part i's schedule into device memory d_sends; fill res from the keys in h_small.
+int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capacity, tacos_result *res,
+                   cudaStream_t st) {
+  Part &pt = pl->parts[i];
+  const uint64_t *hs = pl->h_small + 8 * i;
+  const uint64_t key_ag = hs[0], key_rs = hs[1];
+  const uint64_t *stats = hs + 2;
+  std::memset(res, 0, sizeof(*res));
+  res->visits = stats[0];
+  res->dest_events = stats[1];
+  res->matches = stats[2];
+  res->events = stats[3];
+  res->best_key_ag = key_ag;
+  res->best_key_rs = key_rs;
+  const int32_t st_status = (int32_t)(int64_t)stats[4];
+  const int coll = pl->p.collective;
+  const bool need_rs = coll == TACOS_REDUCE_SCATTER || coll == TACOS_ALL_REDUCE;
+  const bool need_ag = coll != TACOS_REDUCE_SCATTER;
+  if (key_ag == kNoKey || (need_rs && key_rs == kNoKey)) {
+    res->status = st_status ? st_status : TACOS_E_UNREACHABLE;
+    return fail(res->status, "no seed finished the synthesis (status %d)", res->status);
+  }
+  const uint64_t mask = (1ull << kKeySeedBits) - 1ull;
+  const uint64_t T_ag = key_ag >> kKeySeedBits, g_ag = key_ag & mask;
+  uint64_t T_rs = 0, g_rs = g_ag;
+  if (need_rs) {
+    if (pt.symmetric) {
+      T_rs = T_ag;
+    } else {
+      T_rs = key_rs >> kKeySeedBits;
+      g_rs = key_rs & mask;
+    }
+  }
+  res->T_ag = need_ag ? T_ag : 0;
+  res->T_rs = T_rs;
+  res->T = (need_ag ? T_ag : 0) + T_rs;
+  if (res->T >= kMaxTime) return fail(TACOS_E_OVERFLOW, "collective time %llu beyond 2^40", (unsigned long long)res->T);
+  res->seed = pl->p.base_seed + g_ag;
+  res->rs_seed = pl->p.base_seed + g_rs;
+  const uint32_t S = pl->p.n_seeds, off = pl->p.seed_offset;
+  const bool ag_local = g_ag >= off && g_ag < (uint64_t)off + S;
+  const bool rs_local = g_rs >= off && g_rs < (uint64_t)off + S;
+  res->winner_local = (need_ag && ag_local ? 1u : 0u) | (need_rs && rs_local ? 2u : 0u);
+  res->status = TACOS_OK;
+  const uint64_t nsend = sends_per_result(pl, pt);
+  if (nsend == 0) return TACOS_OK;
+  if (capacity < nsend) return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)capacity, (unsigned long long)nsend);
+  const uint64_t M = pt.required;
+  const tacos_topology *t = pt.topo;
+  int rc;
+  uint64_t emitted = 0;
+  if (need_rs && rs_local) {
+    const uint32_t job = pt.symmetric ? (uint32_t)(g_rs - off) : S + (uint32_t)(g_rs - off);
+    const Rec *rec = pt.d_rec + (size_t)job * M;
+    uint32_t nl = 0;
+    if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, pt.symmetric ? t->d_rev : nullptr, T_rs, pt.L,
+                                  d_sends, pl->d_sort, pl->sort_bytes, &nl, st)))
+      return fail(rc, "%s", cuda_error_string());
+    pl->last_launches += nl;
+    emitted += M;
+  }
+  if (need_ag && ag_local) {
+    const Rec *rec = pt.d_rec + (size_t)(g_ag - off) * M;
+    const uint64_t base = coll == TACOS_ALL_REDUCE ? M : 0;
+    if ((rc = launch_emit_ag(rec, M, t->d_src, t->d_dst, pt.d_w, T_rs, d_sends + base, st)))
+      return fail(rc, "%s", cuda_error_string());
+    pl->last_launches += 1;
+    emitted += M;
+  }
+  res->n_sends = emitted;
+  return TACOS_OK;
+}
+}  // namespace
+
+extern "C" int tacos_plan_create(const tacos_topology *topo, const tacos_synth_params *p, tacos_plan **out) {
+  if (!out) return fail(TACOS_E_INVALID_ARG, "null out");
+  const tacos_topology *ts[1] = {topo};
+  try {
+    return plan_build(ts, 1, p, out);
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  } catch (...) {
+    return fail(TACOS_E_INVALID_ARG, "internal error");
+  }
+}
+
+extern "C" void tacos_plan_destroy(tacos_plan *pl) { delete pl; }
+
+extern "C" int tacos_plan_search(tacos_plan *pl, void *stream) {
+  if (!pl) return fail(TACOS_E_INVALID_ARG, "null plan");
+  return plan_search(pl, (cudaStream_t)stream);
+}
+
+extern "C" uint64_t *tacos_plan_best_keys(tacos_plan *pl) { return pl ? pl->parts[0].d_keys : nullptr; }
+
+extern "C" int tacos_plan_emit(tacos_plan *pl, tacos_send *d_sends, uint64_t capacity, tacos_result *result,
+                               void *stream) {
+  if (!pl || !result) return fail(TACOS_E_INVALID_ARG, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = plan_read_small(pl, st);
+  if (rc) return rc;
+  pl->last_launches = 0;
+  return plan_emit_part(pl, 0, d_sends, capacity, result, st);
+}
+
+extern "C" int tacos_plan_stats(tacos_plan *pl, tacos_result *result, void *stream) {
+  if (!pl || !result) return fail(TACOS_E_INVALID_ARG, "null argument");
+  int rc = plan_read_small(pl, (cudaStream_t)stream);
+  if (rc) return rc;
+  const uint64_t *hs = pl->h_small;
+  std::memset(result, 0, sizeof(*result));
+  result->visits = hs[2];
+  result->dest_events = hs[3];
+  result->matches = hs[4];
+  result->events = hs[5];
+  result->status = (int32_t)(int64_t)hs[6];
+  result->best_key_ag = hs[0];
+  result->best_key_rs = hs[1];
+  return TACOS_OK;
+}
+
+extern "C" const uint64_t *tacos_plan_seed_times_device(const tacos_plan *pl, const uint64_t **rs_times) {
+  if (!pl) return nullptr;
+  if (rs_times) *rs_times = pl->parts[0].d_times_rs;
+  return pl->parts[0].d_times_ag;
+}
+
+extern "C" uint32_t tacos_plan_last_launches(const tacos_plan *pl) { return pl ? pl->last_launches : 0; }
+
+// ---------------------------------------------------------------------------
+// one-call synthesis
+// ---------------------------------------------------------------------------
+struct tacos_schedule {
+  tacos_result result{};
+  uint64_t n_sends = 0;
+  tacos_send *sends = nullptr;  // pinned pool block
+  DevBuf host_buf;
+  std::vector<uint64_t> seed_times;
+  ~tacos_schedule() {
+    if (host_buf.p) pinned_pool().release(host_buf.dev, host_buf.p, host_buf.cls);
+  }
+};
+
+extern "C" int tacos_max_sends(const tacos_topology *topo, const tacos_synth_params *p, uint64_t *n_out) {
+  if (!topo || !p || !n_out) return fail(TACOS_E_INVALID_ARG, "null argument");
+  int rc = validate_params(p);
+  if (rc) return rc;
+  uint64_t M;
+  if (p->collective == TACOS_CUSTOM) {
+    const uint32_t W0 = (p->n_chunks + 31u) / 32u;
+    M = 0;
+    for (size_t q = 0; q < (size_t)topo->N * W0; ++q) M += (uint64_t)__builtin_popcount(p->post_bits[q] & ~p->pre_bits[q]);
+  } else {
+    M = (uint64_t)topo->N * p->chunks_per_npu * (uint64_t)(topo->N - 1);
+  }
+  if (p->flags & TACOS_FLAG_NO_SCHEDULE) M = 0;
+  *n_out = p->collective == TACOS_ALL_REDUCE ? 2 * M : M;
+  return TACOS_OK;
+}
+
+namespace {
+bool is_device_ptr(const void *ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Search + emit for n_topos topologies; per topology: sends into dst[i] (host or
+// device, capacity caps[i]) and results[i]; seed times optional.
+int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p, tacos_send **dst,
+               const uint64_t *caps, tacos_result *results, std::vector<uint64_t> *seed_times, cudaStream_t st) {
+  tacos_plan *raw = nullptr;
+  int rc = plan_build(topos, n_topos, p, &raw);
+  if (rc) return rc;
+  std::unique_ptr<tacos_plan> pl(raw);
+  if ((rc = plan_search(pl.get(), st))) return rc;
+  if ((rc = plan_read_small(pl.get(), st))) return rc;
+  for (uint32_t i = 0; i < n_topos; ++i) {
+    const Part &pt = pl->parts[i];
+    const uint64_t need = sends_per_result(pl.get(), pt);
+    if (caps[i] < need) return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)caps[i], (unsigned long long)need);
+    const bool dev_out = need > 0 && is_device_ptr(dst[i]);
+    tacos_send *d_out = dev_out ? dst[i] : nullptr;
+    DevBuf tmp;
+    if (need > 0 && !dev_out) {
+      tmp.dev = pl->device;
+      tmp.p = device_pool().alloc(pl->device, need * sizeof(tacos_send), &tmp.cls);
+      if (!tmp.p) return fail(TACOS_E_NOMEM, "device allocation failed");
+      d_out = reinterpret_cast<tacos_send *>(tmp.p);
+    }
+    rc = plan_emit_part(pl.get(), i, d_out, need, &results[i], st);
+    if (rc == TACOS_OK && need > 0 && !dev_out) {
+      cudaError_t e = cudaMemcpyAsync(dst[i], d_out, need * sizeof(tacos_send), cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "D2H of the schedule: %s", cudaGetErrorString(e));
+    }
+    if (rc == TACOS_OK && seed_times) {
+      seed_times[i].resize(p->n_seeds);
+      cudaError_t e = cudaMemcpyAsync(seed_times[i].data(), pt.d_times_ag, 8 * (size_t)p->n_seeds,
+                                      cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "D2H of seed times: %s", cudaGetErrorString(e));
+    }
+    if (rc == TACOS_OK) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "synchronize: %s", cudaGetErrorString(e));
+    }
+    if (tmp.p) device_pool().release(tmp.dev, tmp.p, tmp.cls);
+    if (rc) return rc;
+    if (seed_times && p->collective == TACOS_ALL_REDUCE && pt.symmetric)
+      for (auto &v : seed_times[i]) v *= 2;  // T_AR(s) = 2 T_AG(s) on a symmetric graph
+  }
+  return TACOS_OK;
+}
+}  // namespace
+
+extern "C" int tacos_synthesize_into(const tacos_topology *topo, const tacos_synth_params *p, tacos_send *sends,
+                                     uint64_t capacity, tacos_result *result, void *stream) {
+  if (!topo || !p || !result) return fail(TACOS_E_INVALID_ARG, "null argument");
+  try {
+    const tacos_topology *ts[1] = {topo};
+    tacos_send *d[1] = {sends};
+    uint64_t caps[1] = {sends ? capacity : 0};
+    return synth_many(ts, 1, p, d, caps, result, nullptr, (cudaStream_t)stream);
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  }
+}
+
+extern "C" int tacos_synthesize_batch(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p,
+                                      tacos_schedule **outs) {
+  if (!topos || !outs || n_topos == 0) return fail(TACOS_E_INVALID_ARG, "null argument");
+  for (uint32_t i = 0; i < n_topos; ++i) outs[i] = nullptr;
+  try {
+    std::vector<std::unique_ptr<tacos_schedule>> sch(n_topos);
+    std::vector<tacos_send *> dst(n_topos, nullptr);
+    std::vector<uint64_t> caps(n_topos, 0);
+    std::vector<tacos_result> res(n_topos);
+    std::vector<std::vector<uint64_t>> times(n_topos);
+    int dev = -1;
+    int rc = cuda_device_ok(&dev);
+    if (rc) return rc;
+    for (uint32_t i = 0; i < n_topos; ++i) {
+      uint64_t n = 0;
+      if (!topos[i]) return fail(TACOS_E_INVALID_ARG, "null topology %u", i);
+      if ((rc = tacos_max_sends(topos[i], p, &n))) return rc;
+      sch[i].reset(new tacos_schedule());
+      if (n) {
+        sch[i]->host_buf.dev = dev;
+        sch[i]->host_buf.p = pinned_pool().alloc(dev, n * sizeof(tacos_send), &sch[i]->host_buf.cls);
+        if (!sch[i]->host_buf.p) return fail(TACOS_E_NOMEM, "pinned allocation failed");
+        sch[i]->sends = reinterpret_cast<tacos_send *>(sch[i]->host_buf.p);
+      }
+      dst[i] = sch[i]->sends;
+      caps[i] = n;
+    }
+    const bool keep = (p->flags & TACOS_FLAG_KEEP_SEED_TIMES) != 0;
+    rc = synth_many(topos, n_topos, p, dst.data(), caps.data(), res.data(), keep ? times.data() : nullptr, nullptr);
+    if (rc) return rc;
+    for (uint32_t i = 0; i < n_topos; ++i) {
+      sch[i]->result = res[i];
+      sch[i]->n_sends = res[i].n_sends;
+      sch[i]->seed_times = std::move(times[i]);
+      outs[i] = sch[i].release();
+    }
+    return TACOS_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  }
+}
+
+extern "C" int tacos_synthesize(const tacos_topology *topo, const tacos_synth_params *p, tacos_schedule **out) {
+  if (out) *out = nullptr;
+  if (!topo || !out) return fail(TACOS_E_INVALID_ARG, "null argument");
+  const tacos_topology *ts[1] = {topo};
+  return tacos_synthesize_batch(ts, 1, p, out);
+}
+
+extern "C" uint64_t tacos_schedule_num_sends(const tacos_schedule *s) { return s ? s->n_sends : 0; }
+extern "C" const tacos_send *tacos_schedule_sends(const tacos_schedule *s) { return s ? s->sends : nullptr; }
+extern "C" uint64_t tacos_schedule_time(const tacos_schedule *s) { return s ? s->result.T : 0; }
+extern "C" uint64_t tacos_schedule_seed(const tacos_schedule *s) { return s ? s->result.seed : 0; }
+extern "C" const tacos_result *tacos_schedule_result(const tacos_schedule *s) { return s ? &s->result : nullptr; }
+extern "C" const uint64_t *tacos_schedule_seed_times(const tacos_schedule *s) {
+  return s && !s->seed_times.empty() ? s->seed_times.data() : nullptr;
+}
+extern "C" void tacos_free_schedule(tacos_schedule *s) { delete s; }
+
+// ---------------------------------------------------------------------------
+// tacos_eval: host replay ("a TEN link matched with a chunk";
+// P:L266-267 arrival before departure; P:L89 postcondition; R8 occupancy)
+// ---------------------------------------------------------------------------
+namespace {
+struct Checker {
+  tacos_eval_report *rep;
+  void add(int kind, uint64_t idx) {
+    rep->per_kind[kind]++;
+    rep->n_violations++;
+    if (rep->first_kind < 0) {
+      rep->first_kind = kind;
+      rep->first_index = idx;
+    }
+  }
+};
+
+// One AG-like phase on orientation o (0: links as given, 1: reversed).
+void check_phase(const tacos_topology *t, const std::vector<uint32_t> &w, int o, const std::vector<tacos_send> &s,
+                 const std::vector<uint64_t> &index, uint32_t C, const std::vector<uint32_t> &pre,
+                 const std::vector<uint32_t> &post, uint32_t W0, Checker &ck) {
+  const uint32_t N = (uint32_t)t->N;
+  const uint64_t kNever = ~0ull;
+  std::vector<uint64_t> arrive((size_t)N * C, kNever);
+  for (uint32_t x = 0; x < N; ++x)
+    for (uint32_t c = 0; c < C; ++c)
+      if ((pre[(size_t)x * W0 + (c >> 5)] >> (c & 31)) & 1u) arrive[(size_t)x * C + c] = 0;
+  std::vector<size_t> ok;
+  ok.reserve(s.size());
+  for (size_t i = 0; i < s.size(); ++i) {
+    const tacos_send &e = s[i];
+    if (e.link >= (uint32_t)t->L || e.chunk >= C || e.src >= N || e.dst >= N) {
+      ck.add(TACOS_V_NO_SUCH_LINK, index[i]);
+      continue;
+    }
+    const uint32_t a = (uint32_t)(o == 0 ? t->src[e.link] : t->dst[e.link]);
+    const uint32_t b = (uint32_t)(o == 0 ? t->dst[e.link] : t->src[e.link]);
+    if (a != e.src || b != e.dst) {
+      ck.add(TACOS_V_NO_SUCH_LINK, index[i]);
+      continue;
+    }
+    if (e.t_end < e.t_start || e.t_end - e.t_start != w[e.link]) ck.add(TACOS_V_WRONG_DURATION, index[i]);
+    ok.push_back(i);
+  }
+  // link intervals disjoint
+  std::vector<size_t> by_link(ok);
+  std::sort(by_link.begin(), by_link.end(), [&](size_t x, size_t y) {
+    return s[x].link != s[y].link ? s[x].link < s[y].link : s[x].t_start < s[y].t_start;
+  });
+  for (size_t j = 1; j < by_link.size(); ++j) {
+    const tacos_send &a = s[by_link[j - 1]], &b = s[by_link[j]];
+    if (a.link == b.link && b.t_start < a.t_end) ck.add(TACOS_V_LINK_OVERLAP, index[by_link[j]]);
+  }
+  // deliveries in arrival order; exactly once
+  std::vector<size_t> by_end(ok);
+  std::stable_sort(by_end.begin(), by_end.end(), [&](size_t x, size_t y) { return s[x].t_end < s[y].t_end; });
+  for (size_t j : by_end) {
+    const tacos_send &e = s[j];
+    uint64_t &a = arrive[(size_t)e.dst * C + e.chunk];
+    if (a != kNever) ck.add(TACOS_V_DUPLICATE_DELIVERY, index[j]);
+    else a = e.t_end;
+  }
+  for (size_t j : ok) {
+    const tacos_send &e = s[j];
+    const uint64_t a = arrive[(size_t)e.src * C + e.chunk];
+    if (a == kNever || a > e.t_start) ck.add(TACOS_V_UNHELD_AT_DEPART, index[j]);
+  }
+  for (uint32_t x = 0; x < N; ++x)
+    for (uint32_t c = 0; c < C; ++c)
+      if (((post[(size_t)x * W0 + (c >> 5)] >> (c & 31)) & 1u) && arrive[(size_t)x * C + c] == kNever)
+        ck.add(TACOS_V_POST_UNMET, (uint64_t)x * C + c);
+}
+}  // namespace
+
+extern "C" int tacos_eval(const tacos_topology *t, const tacos_synth_params *p, const tacos_send *sends,
+                          uint64_t n_sends, tacos_eval_report *out) {
+  if (!t || !p || !out || (!sends && n_sends)) return fail(TACOS_E_INVALID_ARG, "null argument");
+  int rc = validate_params(p);
+  if (rc) return rc;
+  try {
+    std::memset(out, 0, sizeof(*out));
+    out->first_kind = -1;
+    std::vector<uint32_t> w;
+    if ((rc = link_costs(t, p->chunk_bytes, p->time_unit_ns ? p->time_unit_ns : 1u, w))) return rc;
+    const uint32_t N = (uint32_t)t->N;
+    uint32_t C;
+    std::vector<uint32_t> pre, post;
+    uint32_t W0;
+    if (p->collective == TACOS_CUSTOM) {
+      C = p->n_chunks;
+      W0 = (C + 31) / 32;
+      pre.assign(p->pre_bits, p->pre_bits + (size_t)N * W0);
+      post.assign(p->post_bits, p->post_bits + (size_t)N * W0);
+    } else {
+      C = N * p->chunks_per_npu;
+      W0 = (C + 31) / 32;
+      pre.assign((size_t)N * W0, 0u);
+      post.assign((size_t)N * W0, 0u);
+      for (uint32_t x = 0; x < N; ++x)
+        for (uint32_t c = 0; c < C; ++c) {
+          post[(size_t)x * W0 + (c >> 5)] |= 1u << (c & 31);
+          if (c / p->chunks_per_npu == x) pre[(size_t)x * W0 + (c >> 5)] |= 1u << (c & 31);
+        }
+    }
+    Checker ck{out};
+    uint64_t T = 0;
+    for (uint64_t i = 0; i < n_sends; ++i) T = std::max<uint64_t>(T, sends[i].t_end);
+    out->T = T;
+    std::vector<tacos_send> all(sends, sends + n_sends);
+    std::vector<uint64_t> idx(n_sends);
+    for (uint64_t i = 0; i < n_sends; ++i) idx[i] = i;
+    if (p->collective == TACOS_ALL_GATHER || p->collective == TACOS_CUSTOM) {
+      check_phase(t, w, 0, all, idx, C, pre, post, W0, ck);
+      return TACOS_OK;
+    }
+    // RS part (all of an RS; the earliest half of an AR): mirror back into an AG on G^T
+    std::vector<uint64_t> order(n_sends);
+    for (uint64_t i = 0; i < n_sends; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+      return all[a].t_start != all[b].t_start ? all[a].t_start < all[b].t_start : all[a].link < all[b].link;
+    });
+    const uint64_t n_rs = p->collective == TACOS_ALL_REDUCE ? n_sends / 2 : n_sends;
+    uint64_t T_rs = 0;
+    for (uint64_t j = 0; j < n_rs; ++j) T_rs = std::max<uint64_t>(T_rs, all[order[j]].t_end);
+    out->T_rs = T_rs;
+    std::vector<tacos_send> rs(n_rs), ag;
+    std::vector<uint64_t> rs_idx(n_rs), ag_idx;
+    for (uint64_t j = 0; j < n_rs; ++j) {
+      const tacos_send &e = all[order[j]];
+      tacos_send m = e;
+      m.src = e.dst;
+      m.dst = e.src;
+      m.t_start = T_rs - std::min<uint64_t>(T_rs, e.t_end);
+      m.t_end = T_rs - std::min<uint64_t>(T_rs, e.t_start);
+      rs[j] = m;
+      rs_idx[j] = order[j];
+    }
+    check_phase(t, w, 1, rs, rs_idx, C, pre, post, W0, ck);
+    if (p->collective == TACOS_ALL_REDUCE) {
+      for (uint64_t j = n_rs; j < n_sends; ++j) {
+        tacos_send e = all[order[j]];
+        if (e.t_start < T_rs) {
+          ck.add(TACOS_V_PHASE_ORDER, order[j]);
+          continue;
+        }
+        e.t_start -= T_rs;
+        e.t_end -= T_rs;
+        ag.push_back(e);
+        ag_idx.push_back(order[j]);
+      }
+      check_phase(t, w, 0, ag, ag_idx, C, pre, post, W0, ck);
+    }
+    return TACOS_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  }
+}
+
+// ---------------------------------------------------------------------------
+extern "C" const char *tacos_strerror(int code) {
+  switch (code) {
+    case TACOS_OK: return "ok";
+    case TACOS_E_INVALID_ARG: return "invalid argument";
+    case TACOS_E_TOPOLOGY: return "invalid topology";
+    case TACOS_E_UNREACHABLE: return "postcondition unreachable";
+    case TACOS_E_CUDA: return "CUDA error";
+    case TACOS_E_NOMEM: return "out of memory";
+    case TACOS_E_OVERFLOW: return "value out of supported range";
+    case TACOS_E_VERIFY: return "verification failed";
+    case TACOS_E_NCCL: return "NCCL error";
+    case TACOS_E_CAPACITY: return "output buffer too small";
+    default: return "unknown error";
+  }
+}
+extern "C" const char *tacos_last_error(void) { return g_last_error.c_str(); }
+extern "C" int tacos_abi_version(void) { return TACOS_ABI_VERSION; }
+
+extern "C" int tacos_philox_device(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  if (!ctr || !key || !out) return fail(TACOS_E_INVALID_ARG, "null argument");
+  int dev, rc;
+  if ((rc = cuda_device_ok(&dev))) return rc;
+  uint32_t h[6] = {ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1]};
+  uint32_t *d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, 64));
+  cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
+  rc = launch_philox_probe(d, d + 8, nullptr);
+  if (rc == 0) {
+    cudaError_t e = cudaMemcpy(out, d + 8, 16, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "%s", cudaGetErrorString(e));
+  } else {
+    rc = fail(rc, "%s", cuda_error_string());
+  }
+  cudaFree(d);
+  return rc;
+}

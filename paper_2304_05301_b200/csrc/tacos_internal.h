@@ -1,0 +1,89 @@
+// tacos_internal.h -- shared between the host runtime (tacos_api.cpp) and the
+// CUDA kernels (tacos_kernels.cu).  Product side only; the oracle never
+// includes this file.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+
+namespace tacos {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr int kKeySeedBits = 20;              // best key = (T << 20) | global seed index
+constexpr unsigned long long kNoKey = 0x7FFFFFFFFFFFFFFFull;  // no finished seed (also max as int64)
+constexpr uint64_t kMaxTime = 1ull << 40;     // T must stay below 2^40 time units
+constexpr int kMaxVPL = 4;                    // uint4 vectors per lane: C <= 32*4*32*4 = 16384
+constexpr uint32_t kMaxChunks = 32u * 4u * 32u * kMaxVPL;
+
+// Topology as the kernels see it, for one orientation sigma (0 = G, 1 = G^T).
+// Positions p index the links grouped by destination (CSR): in-links of d are
+// positions in_ptr[d] .. in_ptr[d+1]-1, in ascending link id.
+struct DevTopo {
+  uint32_t N, L, C, k;
+  uint32_t Wp;       // padded words per row = 4 * P * VPL
+  uint32_t P, VPL;   // lanes per destination, uint4 vectors per lane
+  uint32_t custom;   // 1: pre/post rows given
+  uint64_t required; // deliveries needed
+  const uint32_t *in_ptr; // [N+1]
+  const uint32_t *p_src;  // [L] source NPU of position p
+  const uint32_t *p_dst;  // [L]
+  const uint32_t *p_w;    // [L] cost in time units
+  const uint32_t *p_lid;  // [L] link id (input index)
+  const uint32_t *pre;    // [N*Wp] custom only
+  const uint32_t *post;   // [N*Wp] custom only
+};
+
+// Compact send record written by the search (16 B): ordered by (t_start, link)
+// within a job.
+struct Rec {
+  uint32_t chunk, link;
+  uint64_t t_start;
+};
+
+struct Job {
+  const DevTopo *topo;   // device pointer
+  uint64_t seed;
+  uint32_t sigma;
+  uint32_t out_slot;
+  Rec *rec;              // nullptr: recording off
+  uint32_t *g_rows;      // global rows (held | have) when they do not fit in smem
+  unsigned char *g_links;// global per-position arrays when they do not fit in smem
+};
+
+struct JobOut {
+  uint64_t T, V, D, M, E;
+  int32_t status;
+  uint32_t pad;
+};
+
+// Byte offsets of the per-block arrays, either in dynamic shared memory or in
+// the job's global scratch (rows / links regions).
+struct Layout {
+  uint32_t rows_bytes;   // 2*N*Wp*4 (held then have)
+  uint32_t links_bytes;  // per-position arrays
+  // within the links region
+  uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv;
+  // always in shared memory, after [rows][links] when those are resident
+  uint32_t off_hver, off_nlive, off_bitmap, off_wpre;
+  uint32_t smem_bytes;   // total dynamic smem
+  uint32_t rows_in_smem, links_in_smem;
+  uint32_t threads;
+};
+
+Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit);
+
+// ---- kernel launch wrappers (tacos_kernels.cu) ----
+int launch_greedy(const Layout &lay, uint32_t P, uint32_t VPL, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, void *stream);
+int launch_best_keys(const JobOut *d_outs, uint32_t n_seeds, uint32_t seed_offset, uint32_t rs_base,
+                     uint32_t has_rs, uint64_t *d_keys, uint64_t *d_stats, uint64_t *d_times_ag,
+                     uint64_t *d_times_rs, void *stream);
+int launch_emit_ag(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
+                   uint64_t shift, void *out_sends, void *stream);
+int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
+                        const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
+                        size_t scratch_bytes, uint32_t *launches, void *stream);
+size_t rs_sort_scratch_bytes(uint64_t M);
+int launch_philox_probe(const uint32_t *d_in, uint32_t *d_out, void *stream);
+
+const char *cuda_error_string();
+
+}  // namespace tacos

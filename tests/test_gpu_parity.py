@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element on the same seeded inputs (BASELINE.json
+north_star: "bit-exact in schedule and in integer collective time").
+
+Compared per case: every seed's finish time, the winning schedule record by
+record (chunk, src, dst, link, t_start, t_end), and the exact counters
+V (free-link visits), D (destination-events), M (matches), E (events).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+
+    assert torch.cuda.is_available()
+    from paper_2304_05301_b200 import build
+
+    build.build()
+    import paper_2304_05301_b200 as T
+
+    T.load_library()
+    return T
+
+
+def oracle_stats(syn):
+    runs = list(syn.ag) + (list(syn.rs) if syn.rs is not syn.ag else [])
+    return (sum(r.V for r in runs), sum(r.D for r in runs), sum(r.M for r in runs), sum(r.E for r in runs))
+
+
+def run_both(T, topo, k, nbytes, coll, seeds, base_seed=0, pre=None, post=None, n_chunks=0):
+    syn = oracle.synthesize(topo, k, nbytes, coll, [(base_seed + s) % 2**64 for s in range(seeds)], pre=pre, post=post,
+                            n_chunks=n_chunks or None)
+    t = T.Topology.from_workload_topology(topo)
+    sch = T.synthesize(t, coll, k, nbytes, seeds, base_seed, keep_seed_times=True, pre=pre, post=post,
+                       n_chunks=n_chunks)
+    return syn, sch, t
+
+
+def assert_parity(syn, sch, coll):
+    r = sch.result
+    assert r["status"] == 0
+    assert r["T"] == syn.T, (r["T"], syn.T)
+    assert r["seed"] == syn.seed
+    if coll in ("RS", "AR"):
+        assert r["rs_seed"] == syn.rs_seed
+        assert r["T_rs"] == syn.T_rs
+    if coll != "RS":
+        assert r["T_ag"] == syn.T_ag
+    # per-seed times (AG times; AR on symmetric graphs: 2 T_AG)
+    want_times = np.array([g.T for g in syn.ag], dtype=np.uint64)
+    if coll == "AR" and syn.rs is syn.ag:  # symmetric graph: T_AR(s) = 2 T_AG(s)
+        want_times = want_times * np.uint64(2)
+    assert np.array_equal(sch.seed_times, want_times)
+    assert (r["visits"], r["dest_events"], r["matches"], r["events"]) == oracle_stats(syn)
+    assert sch.sends.shape == syn.sends.shape
+    assert sch.sends.tobytes() == syn.sends.tobytes()
+
+
+def test_philox_device_known_answers(T):
+    assert T.tacos_philox_device([0, 0, 0, 0], [0, 0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert T.tacos_philox_device([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    for c in ([1, 2, 3, 4], [0xDEADBEEF, 7, 12345, 1]):
+        assert T.tacos_philox_device(c, [99, 0xABCDEF]) == oracle.philox(c, [99, 0xABCDEF])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 5])
+def test_config_parity_all_seeds(T, cfg):
+    wl = W.config(cfg)
+    syn, sch, t = run_both(T, wl.topo, wl.chunks_per_npu, wl.chunk_bytes, wl.collective, wl.n_seeds)
+    assert_parity(syn, sch, wl.collective)
+    rep = T.evaluate(t, sch.sends, wl.collective, wl.chunks_per_npu, wl.chunk_bytes)
+    assert rep["n_violations"] == 0
+
+
+def test_config1_all_collectives(T):
+    wl = W.config(1)
+    for coll in ("AG", "RS", "AR"):
+        syn, sch, _ = run_both(T, wl.topo, 1, wl.chunk_bytes, coll, 17)
+        assert_parity(syn, sch, coll)
+
+
+@pytest.mark.parametrize("shape", ["mesh16x16_k8", "mesh8x16_k64_global_rows", "mesh4x8_k512_vpl4"])
+def test_hetero_mesh_parity(T, shape):
+    """Config 4's shape (X 200 / Y 100 B/ns, 128 KiB chunks) at sizes the
+    oracle finishes quickly; covers shared-memory rows (C=2048), global rows
+    with 2 vectors per lane (C=8192, N=128) and 4 vectors per lane (C=16384)."""
+    x, y, k = {"mesh16x16_k8": (16, 16, 8), "mesh8x16_k64_global_rows": (8, 16, 64),
+               "mesh4x8_k512_vpl4": (4, 8, 512)}[shape]
+    topo = W.mesh2d(x, y, 200, 100)
+    syn, sch, t = run_both(T, topo, k, 128 << 10, "AR", 4)
+    assert_parity(syn, sch, "AR")
+
+
+def test_config4_full_size(T):
+    """Config 4 at full size (1024 NPUs, C = 8192, 16 seeds, global rows):
+    seed 0 is compared bit-exactly with the oracle (about 2 CPU-minutes);
+    every seed's schedule-level properties: M = C(N-1) matches, T >= the
+    per-node bound, and the winning AR schedule verifies."""
+    wl = W.config(4)
+    t = T.Topology.from_workload_topology(wl.topo)
+    sch = T.synthesize(t, "AR", 8, 128 << 10, 16, keep_seed_times=True)
+    r = sch.result
+    C, N = 8192, 1024
+    assert r["matches"] == 16 * C * (N - 1)
+    assert all(int(x) >= 2 * 5_770_000 for x in sch.seed_times)  # 2 x the corner bound
+    rep = T.evaluate(t, sch.sends, "AR", 8, 128 << 10)
+    assert rep["n_violations"] == 0 and rep["T"] == r["T"]
+    one = T.synthesize(t, "AG", 8, 128 << 10, 1, keep_seed_times=True)
+    g = oracle.synthesize(wl.topo, 8, 128 << 10, "AG", [0])
+    assert one.result["T"] == g.T == int(sch.seed_times[0]) // 2
+    assert one.sends.tobytes() == g.sends.tobytes()
+    assert (one.result["visits"], one.result["dest_events"], one.result["events"]) == (g.ag[0].V, g.ag[0].D, g.ag[0].E)
+
+
+@pytest.mark.parametrize("seed", [0, 5, 11])
+def test_asymmetric_graphs_use_transpose_search(T, seed):
+    """R9: on an asymmetric graph the RS is the mirror of an AG searched on
+    G^T (sigma = 1) and the RS / AG winners are chosen independently."""
+    topo = W.random_strongly_connected(9, 20, seed, bws=(25, 50, 100), alphas=(0, 500))
+    for coll in ("RS", "AR"):
+        syn, sch, _ = run_both(T, topo, 2, 1 << 20, coll, 6)
+        assert_parity(syn, sch, coll)
+
+
+@pytest.mark.parametrize("p", [2, 3, 7])
+def test_uni_ring_allreduce(T, p):
+    syn, sch, _ = run_both(T, W.uni_ring(p), 1, 1 << 20, "AR", 3)
+    assert_parity(syn, sch, "AR")
+    assert sch.result["T"] == 2 * (p - 1) * 10986
+
+
+@pytest.mark.parametrize("case", ["E5", "E6", "E7"])
+def test_custom_hand_examples(T, case):
+    n, links, C, pre, post, want = {
+        "E5": (3, [(1, 2, 2), (0, 2, 1)], 1, {0: [0], 1: [0]}, {0: [0], 1: [0], 2: [0]}, 1),
+        "E6": (3, [(2, 1, 2), (1, 0, 1)], 1, {2: [0]}, {0: [0], 1: [0], 2: [0]}, 3),
+        "E7": (3, [(0, 2, 3), (0, 1, 1), (1, 2, 1)], 1, {0: [0]}, {0: [0], 1: [0], 2: [0]}, 3),
+    }[case]
+    # w = alpha with bw = 1 and a 0-byte payload is not allowed (n > 0); use n = 1 byte, bw = 2^31
+    topo = W.Topology(n, np.array([l[0] for l in links], np.int32), np.array([l[1] for l in links], np.int32),
+                      np.array([l[2] - 1 for l in links], np.uint32), np.array([2**31] * len(links), np.uint32))
+    preb = oracle.bits_from_sets(n, C, pre)
+    postb = oracle.bits_from_sets(n, C, post)
+    syn, sch, _ = run_both(T, topo, 1, 1, "CUSTOM", 8, pre=preb, post=postb, n_chunks=C)
+    assert sch.result["T"] == want
+    assert_parity(syn, sch, "CUSTOM")
+
+
+def test_custom_stall_is_unreachable(T):
+    topo = W.Topology(3, np.array([0, 1], np.int32), np.array([1, 2], np.int32), np.array([1, 1], np.uint32),
+                      np.array([1, 1], np.uint32))
+    pre = oracle.bits_from_sets(3, 1, {0: [0]})
+    post = oracle.bits_from_sets(3, 1, {0: [0], 2: [0]})
+    t = T.Topology.from_workload_topology(topo)
+    with pytest.raises(T.TacosError) as e:
+        T.synthesize(t, "CUSTOM", 1, 1, 2, pre=pre, post=post, n_chunks=1)
+    assert e.value.code == T.TACOS_E_UNREACHABLE
+
+
+def test_not_strongly_connected_rejected_before_kernels(T):
+    t = T.Topology(3, [0, 1], [1, 2], [1, 1], [1, 1])
+    with pytest.raises(T.TacosError) as e:
+        T.synthesize(t, "AG", 1, 1 << 20, 1)
+    assert e.value.code == T.TACOS_E_UNREACHABLE
+
+
+@pytest.mark.parametrize("case", ["n2", "ragged_C33", "k3_torus", "hybrid_k2", "big_seed", "fc9"])
+def test_edge_cases(T, case):
+    topo, k, seeds, base = {
+        "n2": (W.bi_ring(2), 5, 4, 0),
+        "ragged_C33": (W.random_strongly_connected(11, 30, 4), 3, 5, 0),
+        "k3_torus": (W.torus([3, 5]), 3, 7, 123),
+        "hybrid_k2": (W.remove_undirected_links(W.switch_hypercube_hybrid(4, 8, 20, 25), 0.05, 2)[0], 2, 9, 0),
+        "big_seed": (W.torus([4, 4]), 1, 3, 2**64 - 2),
+        "fc9": (W.fully_connected(9, 50), 4, 5, 7),
+    }[case]
+    for coll in ("AG", "AR"):
+        syn, sch, _ = run_both(T, topo, k, 300_000, coll, seeds, base)
+        assert_parity(syn, sch, coll)
+
+
+def test_batch_matches_single(T):
+    topos = [W.config(5).topo, W.remove_undirected_links(W.switch_hypercube_hybrid(16, 16, 20, 25), 0.05, 9)[0],
+             W.torus([8, 8, 8]), W.torus([8, 8])]
+    ts = [T.Topology.from_workload_topology(x) for x in topos]
+    batch = T.synthesize_batch(ts, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=8,
+                               keep_seed_times=True)
+    for x, b in zip(ts, batch):
+        one = T.synthesize(x, "AR", 1, 1 << 20, 8, keep_seed_times=True)
+        assert one.result["T"] == b.result["T"] and one.sends.tobytes() == b.sends.tobytes()
+        assert np.array_equal(one.seed_times, b.seed_times)
+
+
+def test_sharded_plans_select_global_winner(T):
+    """Multi-GPU semantics on one GPU: two shards of the seeds (seed_offset),
+    MIN of their keys, emission by the owner == the unsharded synthesis."""
+    import torch
+
+    wl = W.config(2)
+    t = T.Topology.from_workload_topology(wl.topo)
+    full = T.synthesize(t, "AR", 4, 1 << 20, 16)
+    plans = [T.Plan(t, "AR", 4, 1 << 20, 8, 0, off) for off in (0, 8)]
+    st = torch.cuda.current_stream().cuda_stream
+    for pl in plans:
+        pl.search(st)
+    keys = [pl.best_keys_tensor().clone() for pl in plans]
+    gmin = torch.minimum(keys[0], keys[1])
+    got = None
+    for pl in plans:
+        pl.best_keys_tensor().copy_(gmin)
+        out = torch.zeros(pl.n_sends * 32, dtype=torch.uint8, device="cuda")
+        res = pl.emit(out.data_ptr(), pl.n_sends, st)
+        if res["winner_local"] == 3:
+            got = (res, out.cpu().numpy())
+        else:
+            assert res["winner_local"] == 0
+    assert got is not None
+    res, buf = got
+    assert res["T"] == full.result["T"] and res["seed"] == full.result["seed"]
+    assert T.sends_from_bytes(buf).tobytes() == full.sends.tobytes()
+
+
+def test_synthesize_into_host_and_device(T):
+    import torch
+
+    wl = W.config(3)
+    t = T.Topology.from_workload_topology(wl.topo)
+    p, keep = T.make_params("AR", 1, 1 << 20, 4)
+    n = T.max_sends(t, p)
+    host = torch.zeros(n * 32, dtype=torch.uint8).pin_memory()
+    dev = torch.zeros(n * 32, dtype=torch.uint8, device="cuda")
+    r1 = T.synthesize_into(t, p, host.data_ptr(), n, torch.cuda.current_stream().cuda_stream)
+    r2 = T.synthesize_into(t, p, dev.data_ptr(), n, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert r1["T"] == r2["T"] and r1["n_sends"] == n
+    assert host.numpy().tobytes() == dev.cpu().numpy().tobytes()
+    with pytest.raises(T.TacosError) as e:
+        T.synthesize_into(t, p, dev.data_ptr(), n - 1)
+    assert e.value.code == T.TACOS_E_CAPACITY
+
+
+def test_determinism(T):
+    wl = W.config(5)
+    t = T.Topology.from_workload_topology(wl.topo)
+    a = [T.synthesize(t, "AR", 1, 1 << 20, 32) for _ in range(3)]
+    for b in a[1:]:
+        assert b.sends.tobytes() == a[0].sends.tobytes() and b.result == a[0].result
