@@ -288,47 +288,64 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           const uint32_t p = order[b0 + s];
           const uint32_t sp = p_src[p];
           const uint4 *held4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
+          // Chunk order along the row is vector-major: vector v of lane gl holds
+          // words (v*P + gl)*4 .. +3.  Count and scan per vector so the r-th
+          // candidate is the r-th in ascending chunk id (R12).
           uint4 cv[V];
-          uint32_t kl = 0;
+          uint32_t incl[V], tot[V];
+          uint32_t K = 0;
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             cv[v] = andnot4(held4[v * P + gl], hv[v]);  // held[src] & ~have[d] (& post[d])
             if (custom) cv[v] = and4(cv[v], post4[v * P + gl]);
-            kl += popc4(cv[v]);
-          }
-          uint32_t incl = kl;
+            incl[v] = popc4(cv[v]);
 #pragma unroll
-          for (int o = 1; o < P; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(gmask, incl, o, P);
-            if (gl >= (uint32_t)o) incl += y;
+            for (int o = 1; o < P; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(gmask, incl[v], o, P);
+              if (gl >= (uint32_t)o) incl[v] += y;
+            }
+            tot[v] = __shfl_sync(gmask, incl[v], P - 1, P);
+            K += tot[v];
           }
-          const uint32_t K = __shfl_sync(gmask, incl, P - 1, P);
           if (K == 0u) {
             if (gl == 0) seen[p] = hver[sp];
             continue;
           }
           const uint32_t r = __umulhi(pick[p], K);  // floor(u_pick * K / 2^32)
-          const uint32_t excl = incl - kl;
-          const bool mine = (r >= excl) && (r < incl);
+          bool mine = false;
           uint32_t chunk = 0;
-          if (mine) {
-            uint32_t rr = r - excl;
-            bool found = false;
+          {
+            uint32_t rv = r;  // rank within the vector that holds the r-th candidate
+            bool placed = false;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
+              if (!placed) {
+                if (rv < tot[v]) {
+                  placed = true;
+                  const uint32_t kl = popc4(cv[v]);
+                  const uint32_t excl = incl[v] - kl;
+                  if (rv >= excl && rv < incl[v]) {
+                    mine = true;
+                    uint32_t rr = rv - excl;
+                    bool found = false;
 #pragma unroll
-              for (int cpt = 0; cpt < 4; ++cpt) {
-                if (!found) {
-                  const uint32_t word = u4_get(cv[v], cpt);
-                  const uint32_t pc = __popc(word);
-                  if (rr < pc) {
-                    const uint32_t bit = select_bit(word, rr);
-                    chunk = ((uint32_t)(v * P + gl) * 4u + (uint32_t)cpt) * 32u + bit;
-                    u4_or(hv[v], cpt, 1u << bit);  // claim: withheld from d's other in-links
-                    found = true;
-                  } else {
-                    rr -= pc;
+                    for (int cpt = 0; cpt < 4; ++cpt) {
+                      if (!found) {
+                        const uint32_t word = u4_get(cv[v], cpt);
+                        const uint32_t pc = __popc(word);
+                        if (rr < pc) {
+                          const uint32_t bit = select_bit(word, rr);
+                          chunk = ((uint32_t)(v * P + gl) * 4u + (uint32_t)cpt) * 32u + bit;
+                          u4_or(hv[v], cpt, 1u << bit);  // claim: withheld from d's other in-links
+                          found = true;
+                        } else {
+                          rr -= pc;
+                        }
+                      }
+                    }
                   }
+                } else {
+                  rv -= tot[v];
                 }
               }
             }
