@@ -214,6 +214,8 @@ void tacos_plan_destroy(tacos_plan *plan);
  * compute the local best keys into device memory:
  *   keys[0] = min over local seeds of (T_AG(s) << 20) | s   (AR symmetric: T_AG)
  *   keys[1] = same for the RS search on G^T (asymmetric RS/AR), else keys[0]
+ * A seed that did not finish contributes 0x7FFFFFFFFFFFFFFF (max as int64 and
+ * as uint64, so a MIN all-reduce works in either type).
  * where s = seed_offset + i is the global seed index.  A MIN all-reduce of
  * these two uint64 over ranks selects the global winner. */
 int tacos_plan_search(tacos_plan *plan, void *stream);
@@ -226,6 +228,21 @@ uint64_t *tacos_plan_best_keys(tacos_plan *plan);
  * written (result->winner_local bits); an AR's RS phase goes to d_sends[0, M)
  * and its AG phase to d_sends[M, 2M). */
 int tacos_plan_emit(tacos_plan *plan, tacos_send *d_sends, uint64_t capacity, tacos_result *result, void *stream);
+/* Winner of a (possibly all-reduced) pair of best keys. */
+typedef struct {
+  uint64_t T, T_ag, T_rs;       /* T = T_rs + T_ag (R10); a phase absent from the collective has 0 */
+  uint64_t seed_index_ag;       /* global seed index of the AG phase winner */
+  uint64_t seed_index_rs;       /* global seed index of the RS phase winner (= AG winner on a symmetric graph) */
+  uint32_t local;               /* bit 0: AG winner in [seed_offset, seed_offset + n_seeds); bit 1: RS winner */
+  uint32_t reserved;
+} tacos_winner;
+/* Decode best keys (see tacos_plan_search) into the winning seeds and times,
+ * host only (P:L274 best-of-S; R9 symmetric RS = mirror of the AG winner;
+ * R11 ties to the lowest seed index).  `symmetric` as tacos_is_symmetric.
+ * Errors: TACOS_E_UNREACHABLE if a needed key says no seed finished,
+ * TACOS_E_OVERFLOW if T >= 2^40, TACOS_E_INVALID_ARG. */
+int tacos_select_winner(const uint64_t keys[2], int32_t collective, int symmetric, uint32_t seed_offset,
+                        uint32_t n_seeds, tacos_winner *out);
 /* Per-seed finish times (device pointer, n_seeds uint64: AG on G) and, for an
  * asymmetric RS/AR, the RS search times (second pointer, else NULL). */
 const uint64_t *tacos_plan_seed_times_device(const tacos_plan *plan, const uint64_t **rs_times);

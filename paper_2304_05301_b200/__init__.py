@@ -74,6 +74,15 @@ class tacos_result(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class tacos_winner(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_uint64), ("T_ag", ctypes.c_uint64), ("T_rs", ctypes.c_uint64),
+                ("seed_index_ag", ctypes.c_uint64), ("seed_index_rs", ctypes.c_uint64), ("local", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+
+
 class tacos_eval_report(ctypes.Structure):
     _fields_ = [("T", ctypes.c_uint64), ("T_rs", ctypes.c_uint64), ("n_violations", ctypes.c_uint64),
                 ("per_kind", ctypes.c_uint64 * 7), ("first_kind", ctypes.c_int32), ("reserved", ctypes.c_uint32),
@@ -113,6 +122,8 @@ SIGNATURES = {
     "tacos_plan_best_keys": (_VP, [_VP]),
     "tacos_plan_emit": (ctypes.c_int, [_VP, _VP, ctypes.c_uint64, ctypes.POINTER(tacos_result), _VP]),
     "tacos_plan_seed_times_device": (_VP, [_VP, ctypes.POINTER(_VP)]),
+    "tacos_select_winner": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int32, ctypes.c_int,
+                                           ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(tacos_winner)]),
     "tacos_plan_last_launches": (ctypes.c_uint32, [_VP]),
     "tacos_plan_stats": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_result), _VP]),
     "tacos_eval": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_synth_params), _VP, ctypes.c_uint64,
@@ -255,6 +266,23 @@ def tacos_eval(topo_h, params: tacos_synth_params, sends: np.ndarray) -> dict:
     for i, k in enumerate(VIOLATIONS):
         out[k] = rep.per_kind[i]
     return out
+
+
+NO_KEY = 0x7FFFFFFFFFFFFFFF
+
+
+def make_key(T: int, seed_index: int) -> int:
+    """Best-of-S key of one seed: (T << 20) | global seed index."""
+    return (int(T) << KEY_SEED_BITS) | int(seed_index)
+
+
+def tacos_select_winner(keys, collective, symmetric: bool, seed_offset: int, n_seeds: int) -> dict:
+    k = (ctypes.c_uint64 * 2)(*[int(x) & (2**64 - 1) for x in keys])
+    w = tacos_winner()
+    c = COLLECTIVES[collective] if isinstance(collective, str) else int(collective)
+    _check(load_library().tacos_select_winner(k, c, int(bool(symmetric)), seed_offset, n_seeds, ctypes.byref(w)),
+           "tacos_select_winner")
+    return w.as_dict()
 
 
 def tacos_link_costs(topo_h, chunk_bytes: int, time_unit_ns: int = 1) -> np.ndarray:

@@ -679,31 +679,24 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   const int coll = pl->p.collective;
   const bool need_rs = coll == TACOS_REDUCE_SCATTER || coll == TACOS_ALL_REDUCE;
   const bool need_ag = coll != TACOS_REDUCE_SCATTER;
-  if (key_ag == kNoKey || (need_rs && key_rs == kNoKey)) {
+  tacos_winner win;
+  const uint64_t keys[2] = {key_ag, key_rs};
+  int rc0 = tacos_select_winner(keys, coll, pt.symmetric ? 1 : 0, pl->p.seed_offset, pl->p.n_seeds, &win);
+  if (rc0 == TACOS_E_UNREACHABLE) {
     res->status = st_status ? st_status : TACOS_E_UNREACHABLE;
     return fail(res->status, "no seed finished the synthesis (status %d)", res->status);
   }
-  const uint64_t mask = (1ull << kKeySeedBits) - 1ull;
-  const uint64_t T_ag = key_ag >> kKeySeedBits, g_ag = key_ag & mask;
-  uint64_t T_rs = 0, g_rs = g_ag;
-  if (need_rs) {
-    if (pt.symmetric) {
-      T_rs = T_ag;
-    } else {
-      T_rs = key_rs >> kKeySeedBits;
-      g_rs = key_rs & mask;
-    }
-  }
-  res->T_ag = need_ag ? T_ag : 0;
+  if (rc0) return rc0;
+  const uint64_t T_ag = win.T_ag, g_ag = win.seed_index_ag, T_rs = win.T_rs, g_rs = win.seed_index_rs;
+  res->T_ag = T_ag;
   res->T_rs = T_rs;
-  res->T = (need_ag ? T_ag : 0) + T_rs;
-  if (res->T >= kMaxTime) return fail(TACOS_E_OVERFLOW, "collective time %llu beyond 2^40", (unsigned long long)res->T);
-  res->seed = pl->p.base_seed + g_ag;
+  res->T = win.T;
   res->rs_seed = pl->p.base_seed + g_rs;
+  res->seed = need_ag ? pl->p.base_seed + g_ag : res->rs_seed;
   const uint32_t S = pl->p.n_seeds, off = pl->p.seed_offset;
-  const bool ag_local = g_ag >= off && g_ag < (uint64_t)off + S;
-  const bool rs_local = g_rs >= off && g_rs < (uint64_t)off + S;
-  res->winner_local = (need_ag && ag_local ? 1u : 0u) | (need_rs && rs_local ? 2u : 0u);
+  const bool ag_local = (win.local & 1u) != 0;
+  const bool rs_local = (win.local & 2u) != 0;
+  res->winner_local = win.local;
   res->status = TACOS_OK;
   const uint64_t nsend = sends_per_result(pl, pt);
   if (nsend == 0) return TACOS_OK;
@@ -734,6 +727,30 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   return TACOS_OK;
 }
 }  // namespace
+
+extern "C" int tacos_select_winner(const uint64_t keys[2], int32_t collective, int symmetric, uint32_t seed_offset,
+                                   uint32_t n_seeds, tacos_winner *out) {
+  if (!keys || !out) return fail(TACOS_E_INVALID_ARG, "null argument");
+  if (collective < TACOS_ALL_GATHER || collective > TACOS_CUSTOM) return fail(TACOS_E_INVALID_ARG, "bad collective");
+  std::memset(out, 0, sizeof(*out));
+  const bool need_rs = collective == TACOS_REDUCE_SCATTER || collective == TACOS_ALL_REDUCE;
+  const bool need_ag = collective != TACOS_REDUCE_SCATTER;
+  // the RS phase of a symmetric graph is the mirror of the AG winner (R9); else its own search (key 1)
+  const bool rs_own = need_rs && !symmetric;
+  const uint64_t k_ag = keys[0], k_rs = rs_own ? keys[1] : keys[0];
+  if ((need_ag || !rs_own) && k_ag == kNoKey) return fail(TACOS_E_UNREACHABLE, "no AG seed finished");
+  if (rs_own && k_rs == kNoKey) return fail(TACOS_E_UNREACHABLE, "no RS seed finished");
+  const uint64_t mask = (1ull << kKeySeedBits) - 1ull;
+  out->T_ag = need_ag ? (k_ag >> kKeySeedBits) : 0;
+  out->seed_index_ag = k_ag & mask;
+  out->T_rs = need_rs ? (k_rs >> kKeySeedBits) : 0;
+  out->seed_index_rs = need_rs ? (k_rs & mask) : out->seed_index_ag;
+  out->T = out->T_ag + out->T_rs;  // R10: AR = RS then AG
+  if (out->T >= kMaxTime) return fail(TACOS_E_OVERFLOW, "collective time beyond 2^40 time units");
+  auto local = [&](uint64_t g) { return g >= seed_offset && g < (uint64_t)seed_offset + n_seeds; };
+  out->local = (need_ag && local(out->seed_index_ag) ? 1u : 0u) | (need_rs && local(out->seed_index_rs) ? 2u : 0u);
+  return TACOS_OK;
+}
 
 extern "C" int tacos_plan_create(const tacos_topology *topo, const tacos_synth_params *p, tacos_plan **out) {
   if (!out) return fail(TACOS_E_INVALID_ARG, "null out");
