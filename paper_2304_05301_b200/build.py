@@ -10,8 +10,8 @@ INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libtacos.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["tacos_kernels.cu", "tacos_api.cpp"]
-HEADERS = ["tacos_internal.h", os.path.join(INC, "tacos.h")]
+SOURCES = ["tacos_kernels.cu", "tacos_api.cpp"] + [f"greedy_p{p}.cu" for p in (1, 2, 4, 8, 16, 32)]
+HEADERS = ["tacos_internal.h", "tacos_device.cuh", "greedy_kernel.cuh", os.path.join(INC, "tacos.h")]
 
 
 def _stale() -> bool:
@@ -30,6 +30,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(bdir, exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++17", "-I", INC, "-I", CSRC, "-Xcompiler", "-fPIC"]
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(bdir, src + ".o")
         cmd = [NVCC] + ARCH + common + ["-lineinfo", "-c", os.path.join(CSRC, src), "-o", obj]
@@ -37,8 +38,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd += ["-Xptxas", "-v"] if verbose else []
         if verbose:
             print(" ".join(cmd))
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-lpthread", "-ldl", "-lrt"]
     if verbose:

@@ -1,0 +1,398 @@
+// greedy_kernel.cuh -- the TACOS-Greedy search kernel (rows a2-a6 of SURVEY §8).
+//
+// One CTA = one job (seed, orientation sigma) and runs the whole event loop of
+// one greedy All-Gather synthesis (§VI.A, §VI.B),
+// device-resident: no host round trip per event.  Per event, 3 block barriers:
+//
+//   PA  (per link position)  records of the previous event in link-id order;
+//                            arrivals at t: held[dst] |= chunk (R7)
+//       -- barrier --        done test: delivered == required
+//   PM  (per destination,    free in-links (busy_until <= t); exact skip of a
+//        P lanes each)       link whose source is unchanged since its last
+//                            empty visit; Philox draws (R2); shorter-link-first
+//                            order (w, u_ord, link) (R3); then the matching walk:
+//                            have[d] row in registers, per in-link 128-bit loads
+//                            of held[src], andnot + popc, segmented scan over the
+//                            P lanes, r = umulhi(u_pick, K) (R13), branch-free
+//                            rank-select of the r-th candidate, claim (R4)
+//       -- barrier --
+//   PE                       record offsets (link-id bitmap prefix), next event
+//                            time = min busy_until (u64 warp shuffles)
+//       -- barrier --
+//
+// Destinations are independent inside an event (a destination's walk writes
+// only its own in-links' state and its own `have` row; `held` changes only in
+// PA), so PM needs no block barrier between destinations.
+#pragma once
+#include "tacos_device.cuh"
+
+namespace tacos {
+
+template <int V>
+struct ThreadsFor {
+  static constexpr int value = V > 1 ? 512 : 1024;
+};
+
+template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM>
+__global__ void __launch_bounds__(ThreadsFor<V>::value, 1)
+greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Layout lay) {
+  static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long s_min, s_delivered, s_V, s_D, s_M;
+  __shared__ uint32_t s_rec_base, s_next_base;
+
+  const Job job = jobs[blockIdx.x];
+  const DevTopo T = *job.topo;
+  const uint32_t N = T.N, L = T.L, Wp = T.Wp;
+  const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
+  const uint32_t *__restrict__ p_src = T.p_src;
+  const uint32_t *__restrict__ p_dst = T.p_dst;
+  const uint32_t *__restrict__ p_w = T.p_w;
+  const uint32_t *__restrict__ p_lid = T.p_lid;
+  const uint32_t *__restrict__ in_ptr = T.in_ptr;
+  const bool custom = T.custom != 0u;
+
+  uint32_t *held;
+  if constexpr (ROWS_SMEM) held = reinterpret_cast<uint32_t *>(smem);
+  else held = job.g_rows;
+  uint32_t *have = held + (size_t)N * Wp;  // held | pending | claimed (R4)
+  unsigned char *links_base;
+  if constexpr (LINKS_SMEM) links_base = smem + (ROWS_SMEM ? lay.rows_bytes : 0u);
+  else links_base = job.g_links;
+  unsigned long long *busy = reinterpret_cast<unsigned long long *>(links_base + lay.off_busy);
+  uint32_t *cur = reinterpret_cast<uint32_t *>(links_base + lay.off_cur);
+  uint32_t *ord = reinterpret_cast<uint32_t *>(links_base + lay.off_ord);
+  uint32_t *pick = reinterpret_cast<uint32_t *>(links_base + lay.off_pick);
+  uint32_t *seen = reinterpret_cast<uint32_t *>(links_base + lay.off_seen);
+  uint32_t *order = reinterpret_cast<uint32_t *>(links_base + lay.off_order);
+  unsigned char *lv = links_base + lay.off_lv;
+  uint32_t *hver = reinterpret_cast<uint32_t *>(smem + lay.off_hver);
+  uint32_t *bitmap2 = reinterpret_cast<uint32_t *>(smem + lay.off_bitmap);  // 2 x nbw words (event parity)
+  uint32_t *wpre = reinterpret_cast<uint32_t *>(smem + lay.off_wpre);
+  const uint32_t nbw = (L + 31u) / 32u;
+  const uint32_t seed_lo = (uint32_t)job.seed, seed_hi = (uint32_t)(job.seed >> 32);
+  Rec *rec = job.rec;
+
+  // ---- a2: state init (P:L89 precondition; P:L212 start at t = 0) ----
+  const uint32_t NW = N * Wp;
+  for (uint32_t i = tid; i < NW; i += nthr) {
+    uint32_t v;
+    if (custom) {
+      v = __ldg(&T.pre[i]);
+    } else {  // AG: chunks x*k .. x*k+k-1 (R12)
+      const uint32_t x = i / Wp, q = i - x * Wp;
+      const uint32_t lo = x * T.k, hi = lo + T.k, wlo = q * 32u, whi = wlo + 32u;
+      const uint32_t a = lo > wlo ? lo : wlo, b = hi < whi ? hi : whi;
+      v = 0u;
+      if (a < b) v = ((b - a) == 32u ? 0xFFFFFFFFu : ((1u << (b - a)) - 1u)) << (a - wlo);
+    }
+    held[i] = v;
+    have[i] = v;
+  }
+  for (uint32_t p = tid; p < L; p += nthr) {
+    busy[p] = 0ull;
+    cur[p] = kNone;
+    seen[p] = kNone;
+  }
+  for (uint32_t x = tid; x < N; x += nthr) hver[x] = 0u;
+  for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
+  if (tid == 0) {
+    s_delivered = 0ull;
+    s_V = s_D = s_M = 0ull;
+    s_rec_base = 0u;
+    s_next_base = 0u;
+  }
+  __syncthreads();
+
+  unsigned long long t = 0ull, t_prev = 0ull;
+  uint32_t e = 0u, E = 0u;
+  int status = 0;
+  unsigned long long myV = 0, myD = 0, myM = 0;
+
+  const uint32_t gl = lane & (P - 1);
+  const uint32_t gmask = (P == 32) ? 0xFFFFFFFFu : (((1u << P) - 1u) << (lane & ~(uint32_t)(P - 1)));
+  const uint32_t ngroups = nthr / P;
+
+  for (;;) {
+    // ================= PA: previous event's records, arrivals at t =================
+    {
+      const uint32_t rec_base = s_rec_base;
+      const uint32_t *bm_prev = bitmap2 + ((e + 1u) & 1u) * nbw;  // bitmap of event e-1
+      uint32_t arr = 0;
+      for (uint32_t p = tid; p < L; p += nthr) {
+        const uint32_t c = cur[p];
+        if (c == kNone) continue;
+        const unsigned long long b = busy[p];
+        if (rec != nullptr && e > 0u && b - __ldg(&p_w[p]) == t_prev) {
+          const uint32_t lid = __ldg(&p_lid[p]);
+          const uint32_t wi = lid >> 5;
+          const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
+          Rec r;
+          r.chunk = c;
+          r.link = lid;
+          r.t_start = t_prev;
+          rec[idx] = r;
+        }
+        if (b == t) {  // R7: held by dst from this instant
+          const uint32_t d = __ldg(&p_dst[p]);
+          atomicOr(&held[(size_t)d * Wp + (c >> 5)], 1u << (c & 31u));
+          hver[d] = e;
+          cur[p] = kNone;
+          ++arr;
+        }
+      }
+      arr = warp_sum_u32(arr);
+      if (lane == 0 && arr) atomicAdd(&s_delivered, (unsigned long long)arr);
+    }
+    __syncthreads();
+    if (s_delivered == T.required) break;  // done test (postcondition holds)
+    if (tid == 0) {
+      s_rec_base = s_next_base;
+      s_min = ~0ull;
+    }
+    ++E;
+
+    // ================= PM: per-destination draws, order and matching =================
+    {
+      uint32_t *bm = bitmap2 + (e & 1u) * nbw;
+      for (uint32_t d = tid / P; d < N; d += ngroups) {
+        const uint32_t b0 = __ldg(&in_ptr[d]), b1 = __ldg(&in_ptr[d + 1]);
+        // -- free / live in-links and their Philox draws (a4) --
+        uint32_t nfree = 0, nl = 0;
+        for (uint32_t q = b0 + gl; q < b1; q += P) {
+          unsigned char f = 0;
+          if (busy[q] <= t) {  // free: nothing in flight on it
+            ++nfree;
+            f = 1;
+            // exact skip: K stays 0 while src is unchanged since its last empty visit
+            if (seen[q] != hver[__ldg(&p_src[q])]) {
+              const uint4 r = philox4x32_10(
+                  make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
+              ord[q] = r.x;
+              pick[q] = r.y;
+              f = 2;
+              ++nl;
+            }
+          }
+          lv[q] = f;
+        }
+        if (P > 1) {
+          nfree = __reduce_add_sync(gmask, nfree);
+          nl = __reduce_add_sync(gmask, nl);
+        }
+        if (gl == 0) {
+          myV += nfree;
+          myD += nfree ? 1u : 0u;
+        }
+        if (nl == 0u) continue;
+        if (P > 1) __syncwarp(gmask);
+        // -- shorter-link-first order of the live in-links (R3): rank by (w, u_ord, link) --
+        for (uint32_t q = b0 + gl; q < b1; q += P) {
+          if (lv[q] != 2) continue;
+          const uint32_t wq = __ldg(&p_w[q]), oq = ord[q];
+          uint32_t rank = 0;
+          for (uint32_t u = b0; u < b1; ++u) {
+            if (lv[u] != 2) continue;
+            const uint32_t wu = __ldg(&p_w[u]), ou = ord[u];
+            // positions of a destination are in ascending link id: u < q <=> lid_u < lid_q
+            rank += (wu < wq) || (wu == wq && (ou < oq || (ou == oq && u < q)));
+          }
+          order[b0 + rank] = q;
+        }
+        if (P > 1) __syncwarp(gmask);
+        // -- the matching walk (a5) --
+        uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wp);
+        const uint4 *post4 = reinterpret_cast<const uint4 *>(T.post + (size_t)d * Wp);
+        uint4 hv[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+        for (uint32_t s = 0; s < nl; ++s) {
+          const uint32_t p = order[b0 + s];
+          const uint32_t sp = __ldg(&p_src[p]);
+          const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
+          // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
+          uint4 cv[V];
+          uint32_t incl[V], tot[V];
+          uint32_t K = 0;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            cv[v] = andnot4(h4[v * P + gl], hv[v]);  // held[src] & ~have[d]
+            if (custom) cv[v] = and4(cv[v], __ldg(&post4[v * P + gl]));  // & post[d]
+            incl[v] = popc4(cv[v]);
+#pragma unroll
+            for (int o = 1; o < P; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(gmask, incl[v], o, P);
+              if (gl >= (uint32_t)o) incl[v] += y;
+            }
+            tot[v] = (P > 1) ? __shfl_sync(gmask, incl[v], P - 1, P) : incl[v];
+            K += tot[v];
+          }
+          if (K == 0u) {
+            if (gl == 0) seen[p] = hver[sp];
+            continue;
+          }
+          const uint32_t r = __umulhi(pick[p], K);  // floor(u_pick * K / 2^32)
+          // vector holding the r-th candidate, rank inside it
+          uint32_t rv = r;
+          int vsel = 0;
+#pragma unroll
+          for (int v = 0; v + 1 < V; ++v) {
+            const bool adv = (vsel == v) && (rv >= tot[v]);
+            rv = adv ? rv - tot[v] : rv;
+            vsel = adv ? v + 1 : vsel;
+          }
+          uint4 x = cv[0];
+          uint32_t inc = incl[0];
+#pragma unroll
+          for (int v = 1; v < V; ++v) {
+            x = (vsel == v) ? cv[v] : x;
+            inc = (vsel == v) ? incl[v] : inc;
+          }
+          const uint32_t cx = __popc(x.x), cy = __popc(x.y), cz = __popc(x.z);
+          const uint32_t excl = inc - (cx + cy + cz + __popc(x.w));
+          const bool mine = (rv >= excl) && (rv < inc);
+          uint32_t rr = rv - excl;
+          // word inside the lane's vector, branch-free
+          uint32_t wi = 0, word = x.x;
+          bool m = rr >= cx;
+          rr = m ? rr - cx : rr; wi = m ? 1u : wi; word = m ? x.y : word;
+          m = m && rr >= cy;
+          rr = m ? rr - cy : rr; wi = m ? 2u : wi; word = m ? x.z : word;
+          m = m && rr >= cz;
+          rr = m ? rr - cz : rr; wi = m ? 3u : wi; word = m ? x.w : word;
+          const uint32_t bit = select_bit(word, rr);
+          const uint32_t mask = mine ? (1u << bit) : 0u;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {  // claim: withheld from d's other in-links (R4)
+            if (vsel == v) {
+              hv[v].x |= wi == 0u ? mask : 0u;
+              hv[v].y |= wi == 1u ? mask : 0u;
+              hv[v].z |= wi == 2u ? mask : 0u;
+              hv[v].w |= wi == 3u ? mask : 0u;
+            }
+          }
+          uint32_t chunk = (((uint32_t)vsel * P + gl) * 4u + wi) * 32u + bit;
+          if (P > 1) chunk = __shfl_sync(gmask, chunk, __ffs(__ballot_sync(gmask, mine)) - 1);
+          if (gl == 0) {
+            cur[p] = chunk;
+            busy[p] = t + __ldg(&p_w[p]);
+            ++myM;
+            const uint32_t lid = __ldg(&p_lid[p]);
+            atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];
+      }
+    }
+    __syncthreads();
+
+    // ================= PE: record offsets, next event time =================
+    {
+      const uint32_t *bm = bitmap2 + (e & 1u) * nbw;
+      uint32_t *bm_clear = bitmap2 + ((e + 1u) & 1u) * nbw;  // event e-1's map: its records are written
+      if (tid < 32) {
+        uint32_t running = 0;
+        for (uint32_t base = 0; base < nbw; base += 32u) {
+          const uint32_t i = base + lane;
+          const uint32_t v = i < nbw ? __popc(bm[i]) : 0u;
+          uint32_t incl = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+          }
+          if (i < nbw) wpre[i] = running + incl - v;
+          running += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        if (lane == 0) s_next_base = s_rec_base + running;
+      }
+      for (uint32_t i = tid; i < nbw; i += nthr) bm_clear[i] = 0u;
+      unsigned long long mn = ~0ull;
+      for (uint32_t p = tid; p < L; p += nthr)
+        if (cur[p] != kNone) {
+          const unsigned long long b = busy[p];
+          mn = b < mn ? b : mn;
+        }
+      mn = warp_min_u64(mn);
+      if (lane == 0 && mn != ~0ull) atomicMin(&s_min, mn);
+    }
+    __syncthreads();
+    const unsigned long long tn = s_min;
+    if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)
+      status = -3;
+      break;
+    }
+    if (tn >= kMaxTime) {
+      status = -6;
+      break;
+    }
+    t_prev = t;
+    t = tn;
+    ++e;
+  }
+
+  // ---- per-job counters ----
+  myV = warp_sum_u64(myV);
+  myD = warp_sum_u64(myD);
+  myM = warp_sum_u64(myM);
+  if (lane == 0) {
+    if (myV) atomicAdd(&s_V, myV);
+    if (myD) atomicAdd(&s_D, myD);
+    if (myM) atomicAdd(&s_M, myM);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    JobOut o;
+    o.T = t;
+    o.V = s_V;
+    o.D = s_D;
+    o.M = s_M;
+    o.E = E;
+    o.status = status;
+    o.pad = 0;
+    outs[job.out_slot] = o;
+  }
+}
+
+template <int P, int V, bool R, bool K>
+int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
+  auto fn = greedy_kernel<P, V, R, K>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.smem_bytes);
+  if (e != cudaSuccess) {
+    snprintf(cuda_error_buffer(), 256, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return -4;
+  }
+  fn<<<n_jobs, lay.threads, lay.smem_bytes, st>>>(d_jobs, d_outs, lay);
+  return check_launch("greedy_kernel");
+}
+
+template <int P, int V>
+int launch_greedy_pv(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
+  if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true>(lay, d_jobs, n_jobs, d_outs, st);
+  if (lay.links_in_smem) return launch_greedy_one<P, V, false, true>(lay, d_jobs, n_jobs, d_outs, st);
+  return launch_greedy_one<P, V, false, false>(lay, d_jobs, n_jobs, d_outs, st);
+}
+
+// One translation unit per P (greedy_p<P>.cu) instantiates these.
+template <int P>
+int launch_greedy_p(const Layout &lay, uint32_t V, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs,
+                    cudaStream_t st) {
+  switch (V) {
+    case 1: return launch_greedy_pv<P, 1>(lay, d_jobs, n_jobs, d_outs, st);
+    case 2: return launch_greedy_pv<P, 2>(lay, d_jobs, n_jobs, d_outs, st);
+    case 4: return launch_greedy_pv<P, 4>(lay, d_jobs, n_jobs, d_outs, st);
+    default:
+      snprintf(cuda_error_buffer(), 256, "unsupported vectors per lane %u", V);
+      return -1;
+  }
+}
+
+int launch_greedy_p1(const Layout &, uint32_t, const Job *, uint32_t, JobOut *, cudaStream_t);
+int launch_greedy_p2(const Layout &, uint32_t, const Job *, uint32_t, JobOut *, cudaStream_t);
+int launch_greedy_p4(const Layout &, uint32_t, const Job *, uint32_t, JobOut *, cudaStream_t);
+int launch_greedy_p8(const Layout &, uint32_t, const Job *, uint32_t, JobOut *, cudaStream_t);
+int launch_greedy_p16(const Layout &, uint32_t, const Job *, uint32_t, JobOut *, cudaStream_t);
+int launch_greedy_p32(const Layout &, uint32_t, const Job *, uint32_t, JobOut *, cudaStream_t);
+
+}  // namespace tacos

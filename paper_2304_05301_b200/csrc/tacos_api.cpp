@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -449,6 +450,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     const uint32_t W0 = (pt.C + 31u) / 32u;
     const uint32_t vec = (W0 + 3u) / 4u;
     pt.P = std::min<uint32_t>(32u, pow2_at_least(vec));
+    if (const char *env = getenv("TACOS_LANES")) {  // tuning override: lanes per destination row
+      const uint32_t want = (uint32_t)atoi(env);
+      if (want >= 1 && want <= 32 && (want & (want - 1)) == 0 && want < pt.P && (vec + want - 1) / want <= 4)
+        pt.P = want;
+    }
     pt.VPL = (vec + pt.P - 1u) / pt.P;
     if (pt.VPL == 3) pt.VPL = 4;
     if (pt.VPL > (uint32_t)kMaxVPL) return fail(TACOS_E_OVERFLOW, "C too large");

@@ -1,0 +1,66 @@
+// tacos_device.cuh -- device helpers of the product path (Philox, bit select,
+// warp reductions).  Product side only; the oracle has its own Philox.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#include "tacos_internal.h"
+
+namespace tacos {
+
+// last launch error text (thread-local), set by check_launch
+char *cuda_error_buffer();
+int check_launch(const char *what);
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (R2; Salmon et al. SC'11).  Counter (t_lo, t_hi, link, sigma),
+// key (seed_lo, seed_hi); word 0 = order key, word 1 = pick draw.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Position of the r-th (0-based) set bit of x, x having more than r set bits:
+// popc bisection, branch-free (predicated selects).
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t r) {
+  uint32_t pos = 0, c;
+  bool m;
+  c = __popc(x & 0xFFFFu); m = r >= c; r = m ? r - c : r; x = m ? x >> 16 : x; pos += m ? 16u : 0u;
+  c = __popc(x & 0xFFu);   m = r >= c; r = m ? r - c : r; x = m ? x >> 8 : x;  pos += m ? 8u : 0u;
+  c = __popc(x & 0xFu);    m = r >= c; r = m ? r - c : r; x = m ? x >> 4 : x;  pos += m ? 4u : 0u;
+  c = __popc(x & 0x3u);    m = r >= c; r = m ? r - c : r; x = m ? x >> 2 : x;  pos += m ? 2u : 0u;
+  c = x & 1u;              m = r >= c;                                         pos += m ? 1u : 0u;
+  return pos;
+}
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) { return __reduce_add_sync(0xFFFFFFFFu, v); }
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = y < v ? y : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint4 andnot4(uint4 a, uint4 b) {
+  return make_uint4(a.x & ~b.x, a.y & ~b.y, a.z & ~b.z, a.w & ~b.w);
+}
+__device__ __forceinline__ uint4 and4(uint4 a, uint4 b) { return make_uint4(a.x & b.x, a.y & b.y, a.z & b.z, a.w & b.w); }
+__device__ __forceinline__ uint32_t popc4(uint4 a) { return __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w); }
+
+}  // namespace tacos

@@ -63,7 +63,7 @@ struct Layout {
   // within the links region
   uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv;
   // always in shared memory, after [rows][links] when those are resident
-  uint32_t off_hver, off_nlive, off_bitmap, off_wpre;
+  uint32_t off_hver, off_bitmap, off_wpre;  // bitmap: 2 x ceil(L/32) words (event parity)
   uint32_t smem_bytes;   // total dynamic smem
   uint32_t rows_in_smem, links_in_smem;
   uint32_t threads;
