@@ -28,6 +28,8 @@
 
 namespace tacos {
 
+constexpr int kRegDeg = 8;  // in-degree handled in registers by the P == 1 path
+
 template <int V>
 struct ThreadsFor {
   static constexpr int value = V > 1 ? 512 : 1024;
@@ -112,6 +114,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t gl = lane & (P - 1);
   const uint32_t gmask = (P == 32) ? 0xFFFFFFFFu : (((1u << P) - 1u) << (lane & ~(uint32_t)(P - 1)));
   const uint32_t ngroups = nthr / P;
+  const bool pre_draw = lay.pre_draw != 0u;
 
   for (;;) {
     // ================= PA: previous event's records, arrivals at t =================
@@ -152,62 +155,39 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
     ++E;
 
+    // ================= PB (optional): per-position draws by every thread =================
+    // Used when the destination groups leave threads idle (N*P < threads/2):
+    // classification and Philox then run on all warps before PM.
+    if (pre_draw) {
+      for (uint32_t q = tid; q < L; q += nthr) {
+        unsigned char f = 0;
+        if (busy[q] <= t) {
+          f = 1;
+          if (seen[q] != hver[__ldg(&p_src[q])]) {
+            const uint4 r = philox4x32_10(
+                make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
+            ord[q] = r.x;
+            pick[q] = r.y;
+            f = 2;
+          }
+        }
+        lv[q] = f;
+      }
+      __syncthreads();
+    }
+
     // ================= PM: per-destination draws, order and matching =================
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
       for (uint32_t d = tid / P; d < N; d += ngroups) {
         const uint32_t b0 = __ldg(&in_ptr[d]), b1 = __ldg(&in_ptr[d + 1]);
-        // -- free / live in-links and their Philox draws (a4) --
-        uint32_t nfree = 0, nl = 0;
-        for (uint32_t q = b0 + gl; q < b1; q += P) {
-          unsigned char f = 0;
-          if (busy[q] <= t) {  // free: nothing in flight on it
-            ++nfree;
-            f = 1;
-            // exact skip: K stays 0 while src is unchanged since its last empty visit
-            if (seen[q] != hver[__ldg(&p_src[q])]) {
-              const uint4 r = philox4x32_10(
-                  make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
-              ord[q] = r.x;
-              pick[q] = r.y;
-              f = 2;
-              ++nl;
-            }
-          }
-          lv[q] = f;
-        }
-        if (P > 1) {
-          nfree = __reduce_add_sync(gmask, nfree);
-          nl = __reduce_add_sync(gmask, nl);
-        }
-        if (gl == 0) {
-          myV += nfree;
-          myD += nfree ? 1u : 0u;
-        }
-        if (nl == 0u) continue;
-        if (P > 1) __syncwarp(gmask);
-        // -- shorter-link-first order of the live in-links (R3): rank by (w, u_ord, link) --
-        for (uint32_t q = b0 + gl; q < b1; q += P) {
-          if (lv[q] != 2) continue;
-          const uint32_t wq = __ldg(&p_w[q]), oq = ord[q];
-          uint32_t rank = 0;
-          for (uint32_t u = b0; u < b1; ++u) {
-            if (lv[u] != 2) continue;
-            const uint32_t wu = __ldg(&p_w[u]), ou = ord[u];
-            // positions of a destination are in ascending link id: u < q <=> lid_u < lid_q
-            rank += (wu < wq) || (wu == wq && (ou < oq || (ou == oq && u < q)));
-          }
-          order[b0 + rank] = q;
-        }
-        if (P > 1) __syncwarp(gmask);
-        // -- the matching walk (a5) --
+        const uint32_t deg = b1 - b0;
         uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wp);
         const uint4 *post4 = reinterpret_cast<const uint4 *>(T.post + (size_t)d * Wp);
         uint4 hv[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
-        for (uint32_t s = 0; s < nl; ++s) {
-          const uint32_t p = order[b0 + s];
+
+        // One step of the matching walk (a5) on in-link position p with pick draw pk.
+        auto step = [&](uint32_t p, uint32_t pk) {
           const uint32_t sp = __ldg(&p_src[p]);
           const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
@@ -229,9 +209,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
           if (K == 0u) {
             if (gl == 0) seen[p] = hver[sp];
-            continue;
+            return;
           }
-          const uint32_t r = __umulhi(pick[p], K);  // floor(u_pick * K / 2^32)
+          const uint32_t r = __umulhi(pk, K);  // floor(u_pick * K / 2^32)
           // vector holding the r-th candidate, rank inside it
           uint32_t rv = r;
           int vsel = 0;
@@ -280,6 +260,129 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             const uint32_t lid = __ldg(&p_lid[p]);
             atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
           }
+        };
+
+        if (P == 1 && deg <= kRegDeg) {
+          // ---- register path: one thread owns the destination and its <= kRegDeg in-links ----
+          unsigned long long key[kRegDeg];
+          uint32_t pk[kRegDeg];
+          uint32_t live = 0, nfree = 0;
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) {
+            key[j] = 0ull;
+            pk[j] = 0u;
+            if ((uint32_t)j < deg) {
+              const uint32_t q = b0 + j;
+              bool isfree, islive;
+              uint32_t o = 0;
+              if (pre_draw) {
+                const unsigned char f = lv[q];
+                isfree = f != 0;
+                islive = f == 2;
+                if (islive) {
+                  o = ord[q];
+                  pk[j] = pick[q];
+                }
+              } else {
+                isfree = busy[q] <= t;
+                islive = isfree && seen[q] != hver[__ldg(&p_src[q])];
+                if (islive) {
+                  const uint4 r = philox4x32_10(
+                      make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
+                  o = r.x;
+                  pk[j] = r.y;
+                }
+              }
+              nfree += isfree ? 1u : 0u;
+              if (islive) {
+                live |= 1u << j;
+                key[j] = ((unsigned long long)__ldg(&p_w[q]) << 32) | o;  // (w, u_ord), R3
+              }
+            }
+          }
+          myV += nfree;
+          myD += nfree ? 1u : 0u;
+          if (live == 0u) continue;
+          // ranks among live in-links by (w, u_ord, position); positions ascend with link id
+          uint32_t rk[kRegDeg];
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) {
+            uint32_t rnk = 0;
+#pragma unroll
+            for (int i = 0; i < kRegDeg; ++i)
+              if (i != j) rnk += ((live >> i) & 1u) && (key[i] < key[j] || (key[i] == key[j] && i < j));
+            rk[j] = ((live >> j) & 1u) ? rnk : 0xFFu;
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+          const uint32_t nl = __popc(live);
+          for (uint32_t s = 0; s < nl; ++s) {
+            uint32_t jj = 0, pp = 0;
+#pragma unroll
+            for (int j = 0; j < kRegDeg; ++j) {
+              jj = rk[j] == s ? (uint32_t)j : jj;
+              pp = rk[j] == s ? pk[j] : pp;
+            }
+            step(b0 + jj, pp);
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];
+          continue;
+        }
+
+        // ---- shared-memory path: per-position draws, ranks and order ----
+        uint32_t nfree = 0, nl = 0;
+        for (uint32_t q = b0 + gl; q < b1; q += P) {
+          unsigned char f;
+          if (pre_draw) {
+            f = lv[q];
+          } else {
+            f = 0;
+            if (busy[q] <= t) {  // free: nothing in flight on it
+              f = 1;
+              // exact skip: K stays 0 while src is unchanged since its last empty visit
+              if (seen[q] != hver[__ldg(&p_src[q])]) {
+                const uint4 r = philox4x32_10(
+                    make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
+                ord[q] = r.x;
+                pick[q] = r.y;
+                f = 2;
+              }
+            }
+            lv[q] = f;
+          }
+          nfree += f ? 1u : 0u;
+          nl += f == 2 ? 1u : 0u;
+        }
+        if (P > 1) {
+          nfree = __reduce_add_sync(gmask, nfree);
+          nl = __reduce_add_sync(gmask, nl);
+        }
+        if (gl == 0) {
+          myV += nfree;
+          myD += nfree ? 1u : 0u;
+        }
+        if (nl == 0u) continue;
+        if (P > 1) __syncwarp(gmask);
+        // shorter-link-first order of the live in-links (R3): rank by (w, u_ord, link)
+        for (uint32_t q = b0 + gl; q < b1; q += P) {
+          if (lv[q] != 2) continue;
+          const uint32_t wq = __ldg(&p_w[q]), oq = ord[q];
+          uint32_t rank = 0;
+          for (uint32_t u = b0; u < b1; ++u) {
+            if (lv[u] != 2) continue;
+            const uint32_t wu = __ldg(&p_w[u]), ou = ord[u];
+            // positions of a destination are in ascending link id: u < q <=> lid_u < lid_q
+            rank += (wu < wq) || (wu == wq && (ou < oq || (ou == oq && u < q)));
+          }
+          order[b0 + rank] = q;
+        }
+        if (P > 1) __syncwarp(gmask);
+#pragma unroll
+        for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+        for (uint32_t s = 0; s < nl; ++s) {
+          const uint32_t p = order[b0 + s];
+          step(p, pick[p]);
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];

@@ -67,6 +67,7 @@ struct Layout {
   uint32_t smem_bytes;   // total dynamic smem
   uint32_t rows_in_smem, links_in_smem;
   uint32_t threads;
+  uint32_t pre_draw;     // 1: draws per position by all threads before the destination phase
 };
 
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit);

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "greedy_kernel.cuh"
 #include "tacos_device.cuh"
@@ -77,6 +78,8 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   while (th < th_max && th < want) th <<= 1;
   if (th < P) th = P;
   lay.threads = th;
+  lay.pre_draw = (N * P * 2u <= th) ? 1u : 0u;  // destination groups would leave half the threads idle
+  if (const char *env = getenv("TACOS_PRE_DRAW")) lay.pre_draw = (uint32_t)atoi(env);
   return lay;
 }
 
