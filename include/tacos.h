@@ -59,7 +59,7 @@ typedef enum {
   TACOS_E_UNREACHABLE = -3, /* G not strongly connected (AG/RS/AR) or greedy stall (CUSTOM, R17) */
   TACOS_E_CUDA = -4,        /* CUDA runtime error or no usable device */
   TACOS_E_NOMEM = -5,       /* host or device allocation failed */
-  TACOS_E_OVERFLOW = -6,    /* w >= 2^32, time >= 2^40 units, C > 16384, L >= 2^24 ... */
+  TACOS_E_OVERFLOW = -6,    /* w >= 2^32 - 1, time >= 2^40 units, C > 16384, L >= 2^24 ... */
   TACOS_E_VERIFY = -7,      /* internal verification failed */
   TACOS_E_NCCL = -8,        /* reserved: cross-GPU selection failed */
   TACOS_E_CAPACITY = -9     /* caller-provided output buffer too small */

@@ -4,7 +4,7 @@
 // one greedy All-Gather synthesis (§VI.A, §VI.B),
 // device-resident: no host round trip per event.  Per event, 3 block barriers:
 //
-//   PA  (per link position)  records of the previous event in link-id order;
+//   PA  (per destination)    records of the previous event in link-id order;
 //                            arrivals at t: held[dst] |= chunk (R7)
 //       -- barrier --        done test: delivered == required
 //   PM  (per destination,    free in-links (busy_until <= t); exact skip of a
@@ -122,27 +122,33 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       const uint32_t rec_base = s_rec_base;
       const uint32_t *bm_prev = bitmap2 + ((e + 1u) & 1u) * nbw;  // bitmap of event e-1
       uint32_t arr = 0;
-      for (uint32_t p = tid; p < L; p += nthr) {
-        const uint32_t c = cur[p];
-        if (c == kNone) continue;
-        const unsigned long long b = busy[p];
-        if (rec != nullptr && e > 0u && b - __ldg(&p_w[p]) == t_prev) {
-          const uint32_t lid = __ldg(&p_lid[p]);
-          const uint32_t wi = lid >> 5;
-          const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
-          Rec r;
-          r.chunk = c;
-          r.link = lid;
-          r.t_start = t_prev;
-          rec[idx] = r;
+      // one thread per destination: its in-links are contiguous positions, so the
+      // held row is updated without atomics
+      for (uint32_t d = tid; d < N; d += nthr) {
+        const uint32_t b0 = __ldg(&in_ptr[d]), b1 = __ldg(&in_ptr[d + 1]);
+        bool got = false;
+        for (uint32_t p = b0; p < b1; ++p) {
+          const uint32_t c = cur[p];
+          if (c == kNone) continue;
+          const unsigned long long b = busy[p];
+          if (rec != nullptr && e > 0u && b - __ldg(&p_w[p]) == t_prev) {
+            const uint32_t lid = __ldg(&p_lid[p]);
+            const uint32_t wi = lid >> 5;
+            const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
+            Rec r;
+            r.chunk = c;
+            r.link = lid;
+            r.t_start = t_prev;
+            rec[idx] = r;
+          }
+          if (b == t) {  // R7: held by dst from this instant
+            held[(size_t)d * Wp + (c >> 5)] |= 1u << (c & 31u);
+            cur[p] = kNone;
+            got = true;
+            ++arr;
+          }
         }
-        if (b == t) {  // R7: held by dst from this instant
-          const uint32_t d = __ldg(&p_dst[p]);
-          atomicOr(&held[(size_t)d * Wp + (c >> 5)], 1u << (c & 31u));
-          hver[d] = e;
-          cur[p] = kNone;
-          ++arr;
-        }
+        if (got) hver[d] = e;
       }
       arr = warp_sum_u32(arr);
       if (lane == 0 && arr) atomicAdd(&s_delivered, (unsigned long long)arr);
@@ -269,7 +275,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           uint32_t live = 0, nfree = 0;
 #pragma unroll
           for (int j = 0; j < kRegDeg; ++j) {
-            key[j] = 0ull;
+            key[j] = ~0ull;
             pk[j] = 0u;
             if ((uint32_t)j < deg) {
               const uint32_t q = b0 + j;
@@ -308,9 +314,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
           for (int j = 0; j < kRegDeg; ++j) {
             uint32_t rnk = 0;
+            // non-live keys are ~0 > every live key (w < 2^32 - 1 is enforced on the host)
 #pragma unroll
             for (int i = 0; i < kRegDeg; ++i)
-              if (i != j) rnk += ((live >> i) & 1u) && (key[i] < key[j] || (key[i] == key[j] && i < j));
+              if (i != j) rnk += (i < j) ? (key[i] <= key[j]) : (key[i] < key[j]);
             rk[j] = ((live >> j) & 1u) ? rnk : 0xFFu;
           }
 #pragma unroll

@@ -213,7 +213,7 @@ int quantize(uint32_t alpha, uint32_t bw, uint64_t n, uint32_t f, uint32_t *w_ou
   const unsigned __int128 den = (unsigned __int128)bw * (f ? f : 1u);
   const unsigned __int128 q = num / den + (num % den != 0 ? 1 : 0);
   if (q == 0) return TACOS_E_TOPOLOGY;
-  if (q > 0xFFFFFFFFull) return TACOS_E_OVERFLOW;
+  if (q >= 0xFFFFFFFFull) return TACOS_E_OVERFLOW;  // w < 2^32 - 1 (the search packs (w, u_ord) into 64 bits)
   *w_out = (uint32_t)q;
   return TACOS_OK;
 }
@@ -223,7 +223,7 @@ int link_costs(const tacos_topology *t, uint64_t n, uint32_t f, std::vector<uint
   for (int32_t l = 0; l < t->L; ++l) {
     int rc = quantize(t->alpha[l], t->bw[l], n, f, &w[l]);
     if (rc == TACOS_E_TOPOLOGY) return fail(rc, "link %d has zero cost (alpha = n = 0)", l);
-    if (rc == TACOS_E_OVERFLOW) return fail(rc, "link %d cost exceeds 2^32 time units", l);
+    if (rc == TACOS_E_OVERFLOW) return fail(rc, "link %d cost exceeds 2^32 - 2 time units", l);
     if (rc) return fail(rc, "link %d: bad cost", l);
   }
   return TACOS_OK;
