@@ -23,7 +23,16 @@
 // Destinations are independent inside an event (a destination's walk writes
 // only its own in-links' state and its own `have` row; `held` changes only in
 // PA), so PM needs no block barrier between destinations.
+//
+// Thread-block clusters: a job may be split over a cluster of Q CTAs (Q SMs),
+// each owning a contiguous range of destinations (their rows, in-links and
+// link state).  A walk reads held[src] / hver[src] of a source owned by another
+// CTA through distributed shared memory; the delivered count, the next event
+// time and the record bitmap are exchanged with DSMEM atomics; the two
+// event-level barriers become cluster barriers (release/acquire at cluster scope).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "tacos_device.cuh"
 
 namespace tacos {
@@ -43,12 +52,15 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   __shared__ unsigned long long s_min, s_delivered, s_V, s_D, s_M;
   __shared__ uint32_t s_rec_base, s_next_base;
 
-  const Job job = jobs[blockIdx.x];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t Q = cluster.num_blocks();
+  const uint32_t crank = cluster.block_rank();
+  const Job job = jobs[blockIdx.x / Q];
   const DevTopo T = *job.topo;
   const uint32_t N = T.N, L = T.L, Wp = T.Wp;
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
   const uint32_t *__restrict__ p_src = T.p_src;
-  const uint32_t *__restrict__ p_dst = T.p_dst;
   const uint32_t *__restrict__ p_w = T.p_w;
   const uint32_t *__restrict__ p_lid = T.p_lid;
   const uint32_t *__restrict__ in_ptr = T.in_ptr;
@@ -75,9 +87,24 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t seed_lo = (uint32_t)job.seed, seed_hi = (uint32_t)(job.seed >> 32);
   Rec *rec = job.rec;
 
+  // destinations [d_lo, d_hi) and their in-link positions [p_lo, p_hi) belong to this CTA
+  const uint32_t chunkN = (N + Q - 1u) / Q;
+  const uint32_t d_lo = min(N, crank * chunkN), d_hi = min(N, d_lo + chunkN);
+  const uint32_t p_lo = __ldg(&in_ptr[d_lo]), p_hi = __ldg(&in_ptr[d_hi]);
+  auto cluster_barrier = [&]() {
+    if (Q > 1) cluster.sync();
+    else __syncthreads();
+  };
+  // source version of NPU x (owned by CTA x / chunkN)
+  auto hver_of = [&](uint32_t x) -> uint32_t {
+    const uint32_t o = x / chunkN;
+    if (o == crank) return hver[x];
+    return *cluster.map_shared_rank(hver + x, o);
+  };
+
   // ---- a2: state init (P:L89 precondition; P:L212 start at t = 0) ----
   const uint32_t NW = N * Wp;
-  for (uint32_t i = tid; i < NW; i += nthr) {
+  for (uint32_t i = d_lo * Wp + tid; i < d_hi * Wp; i += nthr) {
     uint32_t v;
     if (custom) {
       v = __ldg(&T.pre[i]);
@@ -91,20 +118,22 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     held[i] = v;
     have[i] = v;
   }
-  for (uint32_t p = tid; p < L; p += nthr) {
+  for (uint32_t p = p_lo + tid; p < p_hi; p += nthr) {
     busy[p] = 0ull;
     cur[p] = kNone;
     seen[p] = kNone;
   }
-  for (uint32_t x = tid; x < N; x += nthr) hver[x] = 0u;
+  for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) hver[x] = 0u;
   for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
   if (tid == 0) {
     s_delivered = 0ull;
     s_V = s_D = s_M = 0ull;
     s_rec_base = 0u;
     s_next_base = 0u;
+    s_min = ~0ull;
   }
-  __syncthreads();
+  (void)NW;
+  cluster_barrier();  // peers may read our rows / add to our counters from now on
 
   unsigned long long t = 0ull, t_prev = 0ull;
   uint32_t e = 0u, E = 0u;
@@ -124,7 +153,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       uint32_t arr = 0;
       // one thread per destination: its in-links are contiguous positions, so the
       // held row is updated without atomics
-      for (uint32_t d = tid; d < N; d += nthr) {
+      for (uint32_t d = d_lo + tid; d < d_hi; d += nthr) {
         const uint32_t b0 = __ldg(&in_ptr[d]), b1 = __ldg(&in_ptr[d + 1]);
         bool got = false;
         for (uint32_t p = b0; p < b1; ++p) {
@@ -151,25 +180,27 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         if (got) hver[d] = e;
       }
       arr = warp_sum_u32(arr);
-      if (lane == 0 && arr) atomicAdd(&s_delivered, (unsigned long long)arr);
+      if (lane == 0 && arr) {
+        for (uint32_t r = 0; r < Q; ++r) {
+          unsigned long long *dst = r == crank ? &s_delivered : cluster.map_shared_rank(&s_delivered, r);
+          atomicAdd(dst, (unsigned long long)arr);
+        }
+      }
     }
-    __syncthreads();
+    cluster_barrier();
     if (s_delivered == T.required) break;  // done test (postcondition holds)
-    if (tid == 0) {
-      s_rec_base = s_next_base;
-      s_min = ~0ull;
-    }
+    if (tid == 0) s_rec_base = s_next_base;
     ++E;
 
     // ================= PB (optional): per-position draws by every thread =================
     // Used when the destination groups leave threads idle (N*P < threads/2):
     // classification and Philox then run on all warps before PM.
     if (pre_draw) {
-      for (uint32_t q = tid; q < L; q += nthr) {
+      for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
         unsigned char f = 0;
         if (busy[q] <= t) {
           f = 1;
-          if (seen[q] != hver[__ldg(&p_src[q])]) {
+          if (seen[q] != hver_of(__ldg(&p_src[q]))) {
             const uint4 r = philox4x32_10(
                 make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
             ord[q] = r.x;
@@ -185,7 +216,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     // ================= PM: per-destination draws, order and matching =================
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
-      for (uint32_t d = tid / P; d < N; d += ngroups) {
+      for (uint32_t d = d_lo + tid / P; d < d_hi; d += ngroups) {
         const uint32_t b0 = __ldg(&in_ptr[d]), b1 = __ldg(&in_ptr[d + 1]);
         const uint32_t deg = b1 - b0;
         uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wp);
@@ -195,14 +226,27 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         // One step of the matching walk (a5) on in-link position p with pick draw pk.
         auto step = [&](uint32_t p, uint32_t pk) {
           const uint32_t sp = __ldg(&p_src[p]);
-          const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
+          const uint32_t owner = sp / chunkN;
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
           uint4 cv[V];
+          if (!ROWS_SMEM) {  // rows in HBM/L2, written by other SMs of the cluster: L2-coherent loads
+            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
+#pragma unroll
+            for (int v = 0; v < V; ++v) cv[v] = __ldcg(&h4[v * P + gl]);
+          } else if (owner == crank) {
+            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
+#pragma unroll
+            for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
+          } else {  // source row in a peer CTA's shared memory (DSMEM)
+            const uint4 *h4 = reinterpret_cast<const uint4 *>(cluster.map_shared_rank(held + (size_t)sp * Wp, owner));
+#pragma unroll
+            for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
+          }
           uint32_t incl[V], tot[V];
           uint32_t K = 0;
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            cv[v] = andnot4(h4[v * P + gl], hv[v]);  // held[src] & ~have[d]
+            cv[v] = andnot4(cv[v], hv[v]);  // held[src] & ~have[d]
             if (custom) cv[v] = and4(cv[v], __ldg(&post4[v * P + gl]));  // & post[d]
             incl[v] = popc4(cv[v]);
 #pragma unroll
@@ -214,7 +258,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             K += tot[v];
           }
           if (K == 0u) {
-            if (gl == 0) seen[p] = hver[sp];
+            if (gl == 0) seen[p] = hver_of(sp);
             return;
           }
           const uint32_t r = __umulhi(pk, K);  // floor(u_pick * K / 2^32)
@@ -291,7 +335,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                 }
               } else {
                 isfree = busy[q] <= t;
-                islive = isfree && seen[q] != hver[__ldg(&p_src[q])];
+                islive = isfree && seen[q] != hver_of(__ldg(&p_src[q]));
                 if (islive) {
                   const uint4 r = philox4x32_10(
                       make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
@@ -348,7 +392,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             if (busy[q] <= t) {  // free: nothing in flight on it
               f = 1;
               // exact skip: K stays 0 while src is unchanged since its last empty visit
-              if (seen[q] != hver[__ldg(&p_src[q])]) {
+              if (seen[q] != hver_of(__ldg(&p_src[q]))) {
                 const uint4 r = philox4x32_10(
                     make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
                 ord[q] = r.x;
@@ -397,10 +441,34 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
     __syncthreads();
 
-    // ================= PE: record offsets, next event time =================
+    // ================= PE: next event time, record offsets =================
     {
-      const uint32_t *bm = bitmap2 + (e & 1u) * nbw;
+      uint32_t *bm = bitmap2 + (e & 1u) * nbw;
       uint32_t *bm_clear = bitmap2 + ((e + 1u) & 1u) * nbw;  // event e-1's map: its records are written
+      // (a) publish: own matched links into the peers' bitmaps, own min busy_until everywhere
+      if (Q > 1) {
+        for (uint32_t i = tid; i < nbw; i += nthr) {
+          const uint32_t wbits = bm[i];
+          if (wbits)
+            for (uint32_t r = 0; r < Q; ++r)
+              if (r != crank) atomicOr(cluster.map_shared_rank(bm + i, r), wbits);
+        }
+      }
+      unsigned long long mn = ~0ull;
+      for (uint32_t p = p_lo + tid; p < p_hi; p += nthr)
+        if (cur[p] != kNone) {
+          const unsigned long long b = busy[p];
+          mn = b < mn ? b : mn;
+        }
+      mn = warp_min_u64(mn);
+      if (lane == 0 && mn != ~0ull) {
+        for (uint32_t r = 0; r < Q; ++r) {
+          unsigned long long *dst = r == crank ? &s_min : cluster.map_shared_rank(&s_min, r);
+          atomicMin(dst, mn);
+        }
+      }
+      cluster_barrier();
+      // (b) record offsets of this event from the combined bitmap
       if (tid < 32) {
         uint32_t running = 0;
         for (uint32_t base = 0; base < nbw; base += 32u) {
@@ -418,17 +486,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         if (lane == 0) s_next_base = s_rec_base + running;
       }
       for (uint32_t i = tid; i < nbw; i += nthr) bm_clear[i] = 0u;
-      unsigned long long mn = ~0ull;
-      for (uint32_t p = tid; p < L; p += nthr)
-        if (cur[p] != kNone) {
-          const unsigned long long b = busy[p];
-          mn = b < mn ? b : mn;
-        }
-      mn = warp_min_u64(mn);
-      if (lane == 0 && mn != ~0ull) atomicMin(&s_min, mn);
     }
-    __syncthreads();
     const unsigned long long tn = s_min;
+    __syncthreads();  // wpre / s_next_base ready; everyone has read s_min
+    if (tid == 0) s_min = ~0ull;  // peers add to it only after the next cluster barrier
     if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)
       status = -3;
       break;
@@ -452,7 +513,15 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     if (myM) atomicAdd(&s_M, myM);
   }
   __syncthreads();
-  if (tid == 0) {
+  if (Q > 1) {
+    if (tid == 0 && crank != 0) {
+      atomicAdd(cluster.map_shared_rank(&s_V, 0), s_V);
+      atomicAdd(cluster.map_shared_rank(&s_D, 0), s_D);
+      atomicAdd(cluster.map_shared_rank(&s_M, 0), s_M);
+    }
+    cluster.sync();  // also keeps every CTA's shared memory alive until the peers are done with it
+  }
+  if (tid == 0 && crank == 0) {
     JobOut o;
     o.T = t;
     o.V = s_V;
@@ -473,7 +542,29 @@ int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, Job
     snprintf(cuda_error_buffer(), 256, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return -4;
   }
-  fn<<<n_jobs, lay.threads, lay.smem_bytes, st>>>(d_jobs, d_outs, lay);
+  const uint32_t Q = lay.cluster ? lay.cluster : 1u;
+  if (Q > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_jobs * Q, 1, 1);
+    cfg.blockDim = dim3(lay.threads, 1, 1);
+    cfg.dynamicSmemBytes = lay.smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = Q;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, fn, d_jobs, d_outs, lay);
+    if (e != cudaSuccess) {
+      snprintf(cuda_error_buffer(), 256, "cudaLaunchKernelEx (cluster %u): %s", Q, cudaGetErrorString(e));
+      cudaGetLastError();
+      return -4;
+    }
+  } else {
+    fn<<<n_jobs, lay.threads, lay.smem_bytes, st>>>(d_jobs, d_outs, lay);
+  }
   return check_launch("greedy_kernel");
 }
 

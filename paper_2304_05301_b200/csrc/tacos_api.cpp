@@ -449,10 +449,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     pt.rs_search = need_rs && !pt.symmetric;
     const uint32_t W0 = (pt.C + 31u) / 32u;
     const uint32_t vec = (W0 + 3u) / 4u;
-    pt.P = std::min<uint32_t>(32u, pow2_at_least(vec));
+    pt.P = std::min<uint32_t>(32u, pow2_at_least((vec + 3u) / 4u));  // up to 4 vectors per lane
     if (const char *env = getenv("TACOS_LANES")) {  // tuning override: lanes per destination row
       const uint32_t want = (uint32_t)atoi(env);
-      if (want >= 1 && want <= 32 && (want & (want - 1)) == 0 && want < pt.P && (vec + want - 1) / want <= 4)
+      if (want >= 1 && want <= 32 && (want & (want - 1)) == 0 && want <= pow2_at_least(vec) &&
+          (vec + want - 1) / want <= 4)
         pt.P = want;
     }
     pt.VPL = (vec + pt.P - 1u) / pt.P;
@@ -489,6 +490,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   int smem_optin = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const size_t smem_limit = (size_t)smem_optin > 1024 ? (size_t)smem_optin - 1024 : 0;
+  int n_sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev));
   // re-number jobs in group order
   n_jobs = 0;
   for (size_t gi = 0; gi < order.size();) {
@@ -508,7 +511,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     Group g;
     g.P = P0;
     g.VPL = V0;
-    g.lay = make_layout(maxN, maxL, maxW, P0, V0, smem_limit);
+    g.lay = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, n_jobs - begin, (uint32_t)n_sms);
     g.job_begin = begin;
     g.job_end = n_jobs;
     pl->groups.push_back(g);

@@ -68,9 +68,11 @@ struct Layout {
   uint32_t rows_in_smem, links_in_smem;
   uint32_t threads;
   uint32_t pre_draw;     // 1: draws per position by all threads before the destination phase
+  uint32_t cluster;      // CTAs per job (thread-block cluster size), 1 = one CTA per job
 };
 
-Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit);
+Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,
+                   uint32_t n_sms);
 
 // ---- kernel launch wrappers (tacos_kernels.cu) ----
 int launch_greedy(const Layout &lay, uint32_t P, uint32_t VPL, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, void *stream);

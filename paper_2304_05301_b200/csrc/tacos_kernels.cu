@@ -38,7 +38,8 @@ int check_launch(const char *what) {
 // ---------------------------------------------------------------------------
 // Shared-memory / scratch layout of one search job (see greedy_kernel.cuh).
 // ---------------------------------------------------------------------------
-Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit) {
+Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,
+                   uint32_t n_sms) {
   auto al = [](uint32_t x, uint32_t a) { return (x + a - 1u) / a * a; };
   Layout lay{};
   lay.rows_bytes = al(2u * N * Wp * 4u, 16u);
@@ -78,7 +79,17 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   while (th < th_max && th < want) th <<= 1;
   if (th < P) th = P;
   lay.threads = th;
-  lay.pre_draw = (N * P * 2u <= th) ? 1u : 0u;  // destination groups would leave half the threads idle
+  // Cluster size: split each job over Q CTAs (SMs) while the grid still fits on
+  // the chip and every CTA keeps >= 32 destinations.
+  uint32_t Q = 1;
+  while (Q < 8 && (uint64_t)n_jobs * Q * 2 <= n_sms && N / (Q * 2) >= 32) Q <<= 1;
+  if (const char *env = getenv("TACOS_CLUSTER")) {
+    const uint32_t want = (uint32_t)atoi(env);
+    if (want >= 1 && want <= 8 && (want & (want - 1)) == 0) Q = want;
+  }
+  lay.cluster = Q;
+  const uint32_t n_own = (N + Q - 1) / Q;
+  lay.pre_draw = (n_own * P * 2u <= th) ? 1u : 0u;  // destination groups would leave half the threads idle
   if (const char *env = getenv("TACOS_PRE_DRAW")) lay.pre_draw = (uint32_t)atoi(env);
   return lay;
 }
