@@ -99,7 +99,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   auto hver_of = [&](uint32_t x) -> uint32_t {
     const uint32_t o = x / chunkN;
     if (o == crank) return hver[x];
-    return *cluster.map_shared_rank(hver + x, o);
+    return dsmem_ld(dsmem_addr(hver + x, o));
   };
 
   // ---- a2: state init (P:L89 precondition; P:L212 start at t = 0) ----
@@ -181,9 +181,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       }
       arr = warp_sum_u32(arr);
       if (lane == 0 && arr) {
-        for (uint32_t r = 0; r < Q; ++r) {
-          unsigned long long *dst = r == crank ? &s_delivered : cluster.map_shared_rank(&s_delivered, r);
-          atomicAdd(dst, (unsigned long long)arr);
+        if (Q == 1) {
+          atomicAdd(&s_delivered, (unsigned long long)arr);
+        } else {
+          for (uint32_t r = 0; r < Q; ++r) dsmem_add_u64(dsmem_addr(&s_delivered, r), (unsigned long long)arr);
         }
       }
     }
@@ -238,9 +239,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
           } else {  // source row in a peer CTA's shared memory (DSMEM)
-            const uint4 *h4 = reinterpret_cast<const uint4 *>(cluster.map_shared_rank(held + (size_t)sp * Wp, owner));
+            const uint32_t a = dsmem_addr(held + (size_t)sp * Wp, owner);
 #pragma unroll
-            for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
+            for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(v * P + gl) * 16u);
           }
           uint32_t incl[V], tot[V];
           uint32_t K = 0;
@@ -451,7 +452,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           const uint32_t wbits = bm[i];
           if (wbits)
             for (uint32_t r = 0; r < Q; ++r)
-              if (r != crank) atomicOr(cluster.map_shared_rank(bm + i, r), wbits);
+              if (r != crank) dsmem_or_b32(dsmem_addr(bm + i, r), wbits);
         }
       }
       unsigned long long mn = ~0ull;
@@ -462,9 +463,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         }
       mn = warp_min_u64(mn);
       if (lane == 0 && mn != ~0ull) {
-        for (uint32_t r = 0; r < Q; ++r) {
-          unsigned long long *dst = r == crank ? &s_min : cluster.map_shared_rank(&s_min, r);
-          atomicMin(dst, mn);
+        if (Q == 1) {
+          atomicMin(&s_min, mn);
+        } else {
+          for (uint32_t r = 0; r < Q; ++r) dsmem_min_u64(dsmem_addr(&s_min, r), mn);
         }
       }
       cluster_barrier();
@@ -515,9 +517,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   __syncthreads();
   if (Q > 1) {
     if (tid == 0 && crank != 0) {
-      atomicAdd(cluster.map_shared_rank(&s_V, 0), s_V);
-      atomicAdd(cluster.map_shared_rank(&s_D, 0), s_D);
-      atomicAdd(cluster.map_shared_rank(&s_M, 0), s_M);
+      dsmem_add_u64(dsmem_addr(&s_V, 0), s_V);
+      dsmem_add_u64(dsmem_addr(&s_D, 0), s_D);
+      dsmem_add_u64(dsmem_addr(&s_M, 0), s_M);
     }
     cluster.sync();  // also keeps every CTA's shared memory alive until the peers are done with it
   }
