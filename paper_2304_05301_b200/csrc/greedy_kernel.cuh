@@ -490,6 +490,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       for (uint32_t i = tid; i < nbw; i += nthr) bm_clear[i] = 0u;
     }
     const unsigned long long tn = s_min;
+    if (job.trace != nullptr && tid == 0 && e < kTraceEvents) {
+      unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e) * 4;
+      tr[0] = t;
+      tr[1] = s_delivered;
+      tr[2] = tn;
+      tr[3] = s_next_base - s_rec_base;
+    }
     __syncthreads();  // wpre / s_next_base ready; everyone has read s_min
     if (tid == 0) s_min = ~0ull;  // peers add to it only after the next cluster barrier
     if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)

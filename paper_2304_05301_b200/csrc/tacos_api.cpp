@@ -375,6 +375,7 @@ struct tacos_plan {
   DevBuf h_small_buf;
   std::vector<DevBuf> bufs;
   uint32_t last_launches = 0;
+  unsigned long long *d_trace = nullptr;
   ~tacos_plan() {
     for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
     if (h_small_buf.p) pinned_pool().release(h_small_buf.dev, h_small_buf.p, h_small_buf.cls);
@@ -618,6 +619,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         jb.rec = record ? pt.d_rec + (size_t)j * pt.required : nullptr;
         jb.g_rows = nullptr;
         jb.g_links = nullptr;
+        jb.trace = nullptr;
         if (!g.lay.rows_in_smem) {
           jb.g_rows = reinterpret_cast<uint32_t *>(pl->d_rows + rows_off);
           rows_off += g.lay.rows_bytes;
@@ -628,6 +630,12 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         }
       }
     }
+  }
+  if (getenv("TACOS_TRACE") && !pl->jobs.empty()) {
+    if ((rc = dev_alloc(bufs, dev, 8ull * 4 * kTraceEvents * 8, &vp))) return rc;
+    CUDA_TRY(cudaMemset(vp, 0xFF, 8ull * 4 * kTraceEvents * 8));
+    pl->jobs[0].trace = reinterpret_cast<unsigned long long *>(vp);
+    pl->d_trace = pl->jobs[0].trace;
   }
   if ((rc = upload(bufs, dev, pl->jobs.data(), pl->jobs.size(), &pl->d_jobs))) return rc;
   pl->h_small_buf.dev = dev;
@@ -866,6 +874,18 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   if (rc) return rc;
   std::unique_ptr<tacos_plan> pl(raw);
   if ((rc = plan_search(pl.get(), st))) return rc;
+  if (pl->d_trace) {  // debug dump of job 0's event trace (TACOS_TRACE=path)
+    std::vector<unsigned long long> tr(4ull * kTraceEvents * 8);
+    cudaMemcpy(tr.data(), pl->d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE *f = fopen(getenv("TACOS_TRACE"), "w")) {
+      for (uint32_t r = 0; r < 8; ++r)
+        for (uint32_t ev = 0; ev < kTraceEvents; ++ev) {
+          const unsigned long long *x = &tr[(r * kTraceEvents + ev) * 4];
+          if (x[0] != ~0ull) fprintf(f, "%u %u %llu %llu %llu %llu\n", r, ev, x[0], x[1], x[2], x[3]);
+        }
+      fclose(f);
+    }
+  }
   if ((rc = plan_read_small(pl.get(), st))) return rc;
   for (uint32_t i = 0; i < n_topos; ++i) {
     const Part &pt = pl->parts[i];

@@ -47,7 +47,9 @@ struct Job {
   Rec *rec;              // nullptr: recording off
   uint32_t *g_rows;      // global rows (held | have) when they do not fit in smem
   unsigned char *g_links;// global per-position arrays when they do not fit in smem
+  unsigned long long *trace;  // debug (TACOS_TRACE): per CTA rank, per event {t, delivered, local min, matches}
 };
+constexpr uint32_t kTraceEvents = 4096;
 
 struct JobOut {
   uint64_t T, V, D, M, E;
