@@ -50,6 +50,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_min, s_delivered, s_V, s_D, s_M;
+  // cluster exchange slots, indexed by the writer's rank (plain remote stores, no 64-bit DSMEM atomics)
+  __shared__ unsigned long long s_slot_deliv[8], s_slot_min[8], s_slot_cnt[8][3];
   __shared__ uint32_t s_rec_base, s_next_base;
 
   namespace cg = cooperative_groups;
@@ -180,16 +182,19 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         if (got) hver[d] = e;
       }
       arr = warp_sum_u32(arr);
-      if (lane == 0 && arr) {
-        if (Q == 1) {
-          atomicAdd(&s_delivered, (unsigned long long)arr);
-        } else {
-          for (uint32_t r = 0; r < Q; ++r) dsmem_add_u64(dsmem_addr(&s_delivered, r), (unsigned long long)arr);
-        }
+      if (lane == 0 && arr) atomicAdd(&s_delivered, (unsigned long long)arr);  // own deliveries, cumulative
+      if (Q > 1) {
+        __syncthreads();
+        if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_deliv[crank], tid), s_delivered);
       }
     }
     cluster_barrier();
-    if (s_delivered == T.required) break;  // done test (postcondition holds)
+    unsigned long long delivered = s_delivered;
+    if (Q > 1) {
+      delivered = 0;
+      for (uint32_t r = 0; r < Q; ++r) delivered += s_slot_deliv[r];
+    }
+    if (delivered == T.required) break;  // done test (postcondition holds)
     if (tid == 0) s_rec_base = s_next_base;
     ++E;
 
@@ -462,12 +467,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           mn = b < mn ? b : mn;
         }
       mn = warp_min_u64(mn);
-      if (lane == 0 && mn != ~0ull) {
-        if (Q == 1) {
-          atomicMin(&s_min, mn);
-        } else {
-          for (uint32_t r = 0; r < Q; ++r) dsmem_min_u64(dsmem_addr(&s_min, r), mn);
-        }
+      if (lane == 0 && mn != ~0ull) atomicMin(&s_min, mn);  // own positions
+      if (Q > 1) {
+        __syncthreads();
+        if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid), s_min);
       }
       cluster_barrier();
       // (b) record offsets of this event from the combined bitmap
@@ -489,16 +492,18 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       }
       for (uint32_t i = tid; i < nbw; i += nthr) bm_clear[i] = 0u;
     }
-    const unsigned long long tn = s_min;
+    unsigned long long tn = s_min;
+    if (Q > 1)
+      for (uint32_t r = 0; r < Q; ++r) tn = s_slot_min[r] < tn ? s_slot_min[r] : tn;
     if (job.trace != nullptr && tid == 0 && e < kTraceEvents) {
       unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e) * 4;
       tr[0] = t;
-      tr[1] = s_delivered;
+      tr[1] = delivered;
       tr[2] = tn;
       tr[3] = s_next_base - s_rec_base;
     }
     __syncthreads();  // wpre / s_next_base ready; everyone has read s_min
-    if (tid == 0) s_min = ~0ull;  // peers add to it only after the next cluster barrier
+    if (tid == 0) s_min = ~0ull;  // own-position minimum of the next event
     if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)
       status = -3;
       break;
@@ -523,12 +528,21 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   }
   __syncthreads();
   if (Q > 1) {
-    if (tid == 0 && crank != 0) {
-      dsmem_add_u64(dsmem_addr(&s_V, 0), s_V);
-      dsmem_add_u64(dsmem_addr(&s_D, 0), s_D);
-      dsmem_add_u64(dsmem_addr(&s_M, 0), s_M);
+    if (tid == 0) {
+      const uint32_t a = dsmem_addr(&s_slot_cnt[crank][0], 0);
+      dsmem_st_u64(a, s_V);
+      dsmem_st_u64(a + 8u, s_D);
+      dsmem_st_u64(a + 16u, s_M);
     }
     cluster.sync();  // also keeps every CTA's shared memory alive until the peers are done with it
+    if (tid == 0 && crank == 0) {
+      s_V = s_D = s_M = 0ull;
+      for (uint32_t r = 0; r < Q; ++r) {
+        s_V += s_slot_cnt[r][0];
+        s_D += s_slot_cnt[r][1];
+        s_M += s_slot_cnt[r][2];
+      }
+    }
   }
   if (tid == 0 && crank == 0) {
     JobOut o;

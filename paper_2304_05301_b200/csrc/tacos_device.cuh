@@ -81,12 +81,12 @@ __device__ __forceinline__ uint32_t dsmem_ld(uint32_t addr) {
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
-__device__ __forceinline__ void dsmem_add_u64(uint32_t addr, unsigned long long v) {
-  asm volatile("red.relaxed.cluster.shared::cluster.add.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+__device__ __forceinline__ void dsmem_st_u64(uint32_t addr, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
-__device__ __forceinline__ void dsmem_min_u64(uint32_t addr, unsigned long long v) {
-  asm volatile("red.relaxed.cluster.shared::cluster.min.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
-}
+// 64-bit min/add on distributed shared memory are not used: on sm_100a a
+// remote red.min.u64 was observed to be lost (measured), so 64-bit values are
+// exchanged through per-rank slots written with plain remote stores.
 __device__ __forceinline__ void dsmem_or_b32(uint32_t addr, uint32_t v) {
   asm volatile("red.relaxed.cluster.shared::cluster.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
