@@ -146,8 +146,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t gmask = (P == 32) ? 0xFFFFFFFFu : (((1u << P) - 1u) << (lane & ~(uint32_t)(P - 1)));
   const uint32_t ngroups = nthr / P;
   const bool pre_draw = lay.pre_draw != 0u;
+  const bool tracing = job.trace != nullptr && tid == 0;
 
   for (;;) {
+    long long ts[9];  // debug phase timestamps (TACOS_TRACE), thread 0
+    if (tracing) ts[0] = clock64();
     // ================= PA: previous event's records, arrivals at t =================
     {
       const uint32_t rec_base = s_rec_base;
@@ -188,7 +191,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_deliv[crank], tid), s_delivered);
       }
     }
+    if (tracing) ts[1] = clock64();
     cluster_barrier();
+    if (tracing) ts[2] = clock64();
     unsigned long long delivered = s_delivered;
     if (Q > 1) {
       delivered = 0;
@@ -218,6 +223,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       }
       __syncthreads();
     }
+    if (tracing) ts[3] = clock64();
 
     // ================= PM: per-destination draws, order and matching =================
     {
@@ -445,7 +451,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];
       }
     }
+    if (tracing) ts[4] = clock64();
     __syncthreads();
+    if (tracing) ts[5] = clock64();
 
     // ================= PE: next event time, record offsets =================
     {
@@ -472,7 +480,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         __syncthreads();
         if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid), s_min);
       }
+      if (tracing) ts[6] = clock64();
       cluster_barrier();
+      if (tracing) ts[7] = clock64();
       // (b) record offsets of this event from the combined bitmap
       if (tid < 32) {
         uint32_t running = 0;
@@ -495,14 +505,16 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     unsigned long long tn = s_min;
     if (Q > 1)
       for (uint32_t r = 0; r < Q; ++r) tn = s_slot_min[r] < tn ? s_slot_min[r] : tn;
-    if (job.trace != nullptr && tid == 0 && e < kTraceEvents) {
-      unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e) * 4;
+    __syncthreads();  // wpre / s_next_base ready; everyone has read s_min
+    if (tracing && e < kTraceEvents) {
+      ts[8] = clock64();
+      unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e) * kTraceWords;
       tr[0] = t;
       tr[1] = delivered;
       tr[2] = tn;
       tr[3] = s_next_base - s_rec_base;
+      for (int i = 1; i < 9; ++i) tr[3 + i] = (unsigned long long)(ts[i] - ts[i - 1]);
     }
-    __syncthreads();  // wpre / s_next_base ready; everyone has read s_min
     if (tid == 0) s_min = ~0ull;  // own-position minimum of the next event
     if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)
       status = -3;

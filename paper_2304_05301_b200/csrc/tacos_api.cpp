@@ -632,8 +632,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     }
   }
   if (getenv("TACOS_TRACE") && !pl->jobs.empty()) {
-    if ((rc = dev_alloc(bufs, dev, 8ull * 4 * kTraceEvents * 8, &vp))) return rc;
-    CUDA_TRY(cudaMemset(vp, 0xFF, 8ull * 4 * kTraceEvents * 8));
+    if ((rc = dev_alloc(bufs, dev, 8ull * kTraceWords * kTraceEvents * 8, &vp))) return rc;
+    CUDA_TRY(cudaMemset(vp, 0xFF, 8ull * kTraceWords * kTraceEvents * 8));
     pl->jobs[0].trace = reinterpret_cast<unsigned long long *>(vp);
     pl->d_trace = pl->jobs[0].trace;
   }
@@ -875,13 +875,16 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   std::unique_ptr<tacos_plan> pl(raw);
   if ((rc = plan_search(pl.get(), st))) return rc;
   if (pl->d_trace) {  // debug dump of job 0's event trace (TACOS_TRACE=path)
-    std::vector<unsigned long long> tr(4ull * kTraceEvents * 8);
+    std::vector<unsigned long long> tr((size_t)kTraceWords * kTraceEvents * 8);
     cudaMemcpy(tr.data(), pl->d_trace, tr.size() * 8, cudaMemcpyDeviceToHost);
     if (FILE *f = fopen(getenv("TACOS_TRACE"), "w")) {
       for (uint32_t r = 0; r < 8; ++r)
         for (uint32_t ev = 0; ev < kTraceEvents; ++ev) {
-          const unsigned long long *x = &tr[(r * kTraceEvents + ev) * 4];
-          if (x[0] != ~0ull) fprintf(f, "%u %u %llu %llu %llu %llu\n", r, ev, x[0], x[1], x[2], x[3]);
+          const unsigned long long *x = &tr[(r * kTraceEvents + ev) * kTraceWords];
+          if (x[0] == ~0ull) continue;
+          fprintf(f, "%u %u", r, ev);
+          for (uint32_t w = 0; w < kTraceWords; ++w) fprintf(f, " %llu", x[w]);
+          fprintf(f, "\n");
         }
       fclose(f);
     }
