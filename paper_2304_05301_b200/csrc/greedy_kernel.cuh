@@ -82,6 +82,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *seen = reinterpret_cast<uint32_t *>(links_base + lay.off_seen);
   uint32_t *order = reinterpret_cast<uint32_t *>(links_base + lay.off_order);
   unsigned char *lv = links_base + lay.off_lv;
+  // per-position topology (source, cost, link id): staged into shared memory with the link state
+  const uint32_t *t_src = p_src, *t_w = p_w, *t_lid = p_lid;
+  if constexpr (LINKS_SMEM) {
+    t_src = reinterpret_cast<const uint32_t *>(links_base + lay.off_tsrc);
+    t_w = reinterpret_cast<const uint32_t *>(links_base + lay.off_tw);
+    t_lid = reinterpret_cast<const uint32_t *>(links_base + lay.off_tlid);
+  }
   uint32_t *hver = reinterpret_cast<uint32_t *>(smem + lay.off_hver);
   uint32_t *bitmap2 = reinterpret_cast<uint32_t *>(smem + lay.off_bitmap);  // 2 x nbw words (event parity)
   uint32_t *wpre = reinterpret_cast<uint32_t *>(smem + lay.off_wpre);
@@ -124,6 +131,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     busy[p] = 0ull;
     cur[p] = kNone;
     seen[p] = kNone;
+    if constexpr (LINKS_SMEM) {
+      const_cast<uint32_t *>(t_src)[p] = __ldg(&p_src[p]);
+      const_cast<uint32_t *>(t_w)[p] = __ldg(&p_w[p]);
+      const_cast<uint32_t *>(t_lid)[p] = __ldg(&p_lid[p]);
+    }
   }
   for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) hver[x] = 0u;
   for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
@@ -165,8 +177,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           const uint32_t c = cur[p];
           if (c == kNone) continue;
           const unsigned long long b = busy[p];
-          if (rec != nullptr && e > 0u && b - __ldg(&p_w[p]) == t_prev) {
-            const uint32_t lid = __ldg(&p_lid[p]);
+          if (rec != nullptr && e > 0u && b - t_w[p] == t_prev) {
+            const uint32_t lid = t_lid[p];
             const uint32_t wi = lid >> 5;
             const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
             Rec r;
@@ -211,9 +223,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         unsigned char f = 0;
         if (busy[q] <= t) {
           f = 1;
-          if (seen[q] != hver_of(__ldg(&p_src[q]))) {
+          if (seen[q] != hver_of(t_src[q])) {
             const uint4 r = philox4x32_10(
-                make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
+                make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
             ord[q] = r.x;
             pick[q] = r.y;
             f = 2;
@@ -237,7 +249,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 
         // One step of the matching walk (a5) on in-link position p with pick draw pk.
         auto step = [&](uint32_t p, uint32_t pk) {
-          const uint32_t sp = __ldg(&p_src[p]);
+          const uint32_t sp = t_src[p];
           const uint32_t owner = sp / chunkN;
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
           uint4 cv[V];
@@ -317,9 +329,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           if (P > 1) chunk = __shfl_sync(gmask, chunk, __ffs(__ballot_sync(gmask, mine)) - 1);
           if (gl == 0) {
             cur[p] = chunk;
-            busy[p] = t + __ldg(&p_w[p]);
+            busy[p] = t + t_w[p];
             ++myM;
-            const uint32_t lid = __ldg(&p_lid[p]);
+            const uint32_t lid = t_lid[p];
             atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
           }
         };
@@ -347,10 +359,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                 }
               } else {
                 isfree = busy[q] <= t;
-                islive = isfree && seen[q] != hver_of(__ldg(&p_src[q]));
+                islive = isfree && seen[q] != hver_of(t_src[q]);
                 if (islive) {
                   const uint4 r = philox4x32_10(
-                      make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
+                      make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
                   o = r.x;
                   pk[j] = r.y;
                 }
@@ -358,7 +370,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               nfree += isfree ? 1u : 0u;
               if (islive) {
                 live |= 1u << j;
-                key[j] = ((unsigned long long)__ldg(&p_w[q]) << 32) | o;  // (w, u_ord), R3
+                key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
               }
             }
           }
@@ -404,9 +416,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             if (busy[q] <= t) {  // free: nothing in flight on it
               f = 1;
               // exact skip: K stays 0 while src is unchanged since its last empty visit
-              if (seen[q] != hver_of(__ldg(&p_src[q]))) {
+              if (seen[q] != hver_of(t_src[q])) {
                 const uint4 r = philox4x32_10(
-                    make_uint4((uint32_t)t, (uint32_t)(t >> 32), __ldg(&p_lid[q]), job.sigma), seed_lo, seed_hi);
+                    make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
                 ord[q] = r.x;
                 pick[q] = r.y;
                 f = 2;
@@ -430,11 +442,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         // shorter-link-first order of the live in-links (R3): rank by (w, u_ord, link)
         for (uint32_t q = b0 + gl; q < b1; q += P) {
           if (lv[q] != 2) continue;
-          const uint32_t wq = __ldg(&p_w[q]), oq = ord[q];
+          const uint32_t wq = t_w[q], oq = ord[q];
           uint32_t rank = 0;
           for (uint32_t u = b0; u < b1; ++u) {
             if (lv[u] != 2) continue;
-            const uint32_t wu = __ldg(&p_w[u]), ou = ord[u];
+            const uint32_t wu = t_w[u], ou = ord[u];
             // positions of a destination are in ascending link id: u < q <=> lid_u < lid_q
             rank += (wu < wq) || (wu == wq && (ou < oq || (ou == oq && u < q)));
           }

@@ -50,6 +50,9 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   lay.off_pick = o; o += al(L * 4u, 16u);
   lay.off_seen = o; o += al(L * 4u, 16u);
   lay.off_order = o; o += al(L * 4u, 16u);
+  lay.off_tsrc = o; o += al(L * 4u, 16u);
+  lay.off_tw = o; o += al(L * 4u, 16u);
+  lay.off_tlid = o; o += al(L * 4u, 16u);
   lay.off_lv = o; o += al(L, 16u);
   lay.links_bytes = o;
   const uint32_t nbw = (L + 31u) / 32u;
