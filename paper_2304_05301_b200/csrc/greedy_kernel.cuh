@@ -92,6 +92,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *hver = reinterpret_cast<uint32_t *>(smem + lay.off_hver);
   uint32_t *bitmap2 = reinterpret_cast<uint32_t *>(smem + lay.off_bitmap);  // 2 x nbw words (event parity)
   uint32_t *wpre = reinterpret_cast<uint32_t *>(smem + lay.off_wpre);
+  uint32_t *s_inptr = reinterpret_cast<uint32_t *>(smem + lay.off_inptr);  // CSR offsets, own range
   const uint32_t nbw = (L + 31u) / 32u;
   const uint32_t seed_lo = (uint32_t)job.seed, seed_hi = (uint32_t)(job.seed >> 32);
   Rec *rec = job.rec;
@@ -138,6 +139,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
   }
   for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) hver[x] = 0u;
+  for (uint32_t x = d_lo + tid; x <= d_hi; x += nthr) s_inptr[x] = __ldg(&in_ptr[x]);
   for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
   if (tid == 0) {
     s_delivered = 0ull;
@@ -171,7 +173,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       // one thread per destination: its in-links are contiguous positions, so the
       // held row is updated without atomics
       for (uint32_t d = d_lo + tid; d < d_hi; d += nthr) {
-        const uint32_t b0 = __ldg(&in_ptr[d]), b1 = __ldg(&in_ptr[d + 1]);
+        const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         bool got = false;
         for (uint32_t p = b0; p < b1; ++p) {
           const uint32_t c = cur[p];
@@ -241,7 +243,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
       for (uint32_t d = d_lo + tid / P; d < d_hi; d += ngroups) {
-        const uint32_t b0 = __ldg(&in_ptr[d]), b1 = __ldg(&in_ptr[d + 1]);
+        const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         const uint32_t deg = b1 - b0;
         uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wp);
         const uint4 *post4 = reinterpret_cast<const uint4 *>(T.post + (size_t)d * Wp);

@@ -67,7 +67,7 @@ struct Layout {
   uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv;
   uint32_t off_tsrc, off_tw, off_tlid;  // per-position topology copies (src, w, link id)
   // always in shared memory, after [rows][links] when those are resident
-  uint32_t off_hver, off_bitmap, off_wpre;  // bitmap: 2 x ceil(L/32) words (event parity)
+  uint32_t off_hver, off_bitmap, off_wpre, off_inptr;  // bitmap: 2 x ceil(L/32) words (event parity)
   uint32_t smem_bytes;   // total dynamic smem
   uint32_t rows_in_smem, links_in_smem;
   uint32_t threads;
