@@ -39,7 +39,7 @@ UNIT = "matches/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--seeds", type=int, default=0, help="seeds per GPU (default: the config's)")
@@ -297,6 +297,14 @@ def run_gpu(args):
             peaks = json.load(fh)
     except OSError:
         pass
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh).get(wl.name)
+            if tr:
+                traffic = float(tr["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
@@ -354,7 +362,7 @@ def run_gpu(args):
             "winner_seed": res["seed"], "matches_per_step": m_total, "n_sends": n_sends,
             "paper_context": "TACOS-Greedy 512-NPU AR synthesis 6.09 min (P:L354, Ring_FC_Switch, hardware not stated)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": "greedy_kernel (+best_keys)", "peak_source": peak_src,
+                         "traffic": traffic, "kernel": "greedy_kernel (+best_keys)", "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": B},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
