@@ -41,7 +41,7 @@ constexpr int kRegDeg = 8;  // in-degree handled in registers by the P == 1 path
 
 template <int V>
 struct ThreadsFor {
-  static constexpr int value = V > 1 ? 512 : 1024;
+  static constexpr int value = V > 1 ? 512 : 768;  // registers: <= 128 resp. <= 85 per thread
 };
 
 template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM>
@@ -338,16 +338,19 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
         };
 
-        if (P == 1 && deg <= kRegDeg) {
-          // ---- register path: one thread owns the destination and its <= kRegDeg in-links ----
-          unsigned long long key[kRegDeg];
-          uint32_t pk[kRegDeg];
-          uint32_t live = 0, nfree = 0;
+        if (P <= 8 && deg <= (uint32_t)kRegDeg) {
+          // ---- register path: the group owns the destination's <= kRegDeg in-links, in-link j
+          //      in slot j / P of lane j % P; ranks and the walk order stay in registers ----
+          constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
+          unsigned long long key[SL];
+          uint32_t pk[SL];
+          uint32_t nfree = 0, nlive = 0;
 #pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) {
-            key[j] = ~0ull;
-            pk[j] = 0u;
-            if ((uint32_t)j < deg) {
+          for (int sl = 0; sl < SL; ++sl) {
+            key[sl] = ~0ull;
+            pk[sl] = 0u;
+            const uint32_t j = (uint32_t)sl * P + gl;
+            if (j < deg) {
               const uint32_t q = b0 + j;
               bool isfree, islive;
               uint32_t o = 0;
@@ -357,7 +360,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                 islive = f == 2;
                 if (islive) {
                   o = ord[q];
-                  pk[j] = pick[q];
+                  pk[sl] = pick[q];
                 }
               } else {
                 isfree = busy[q] <= t;
@@ -366,39 +369,59 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                   const uint4 r = philox4x32_10(
                       make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
                   o = r.x;
-                  pk[j] = r.y;
+                  pk[sl] = r.y;
                 }
               }
               nfree += isfree ? 1u : 0u;
               if (islive) {
-                live |= 1u << j;
-                key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
+                ++nlive;
+                key[sl] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
               }
             }
           }
-          myV += nfree;
-          myD += nfree ? 1u : 0u;
-          if (live == 0u) continue;
-          // ranks among live in-links by (w, u_ord, position); positions ascend with link id
-          uint32_t rk[kRegDeg];
+          if (P > 1) {
+            nfree = __reduce_add_sync(gmask, nfree);
+            nlive = __reduce_add_sync(gmask, nlive);
+          }
+          if (gl == 0) {
+            myV += nfree;
+            myD += nfree ? 1u : 0u;
+          }
+          if (nlive == 0u) continue;
+          // ranks among live in-links by (w, u_ord, position); positions ascend with link id.
+          // Non-live keys are ~0 > every live key (w < 2^32 - 1 is enforced on the host).
+          uint32_t rk[SL];
 #pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) {
-            uint32_t rnk = 0;
-            // non-live keys are ~0 > every live key (w < 2^32 - 1 is enforced on the host)
+          for (int sl = 0; sl < SL; ++sl) rk[sl] = 0u;
 #pragma unroll
-            for (int i = 0; i < kRegDeg; ++i)
-              if (i != j) rnk += (i < j) ? (key[i] <= key[j]) : (key[i] < key[j]);
-            rk[j] = ((live >> j) & 1u) ? rnk : 0xFFu;
+          for (int i = 0; i < kRegDeg; ++i) {
+            const int isl = i / P, ilane = i % P;
+            const unsigned long long ki =
+                (P > 1) ? __shfl_sync(gmask, key[isl], ilane, P) : key[isl];
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl) {
+              const uint32_t j = (uint32_t)sl * P + gl;
+              rk[sl] += (ki < key[sl] || (ki == key[sl] && (uint32_t)i < j)) ? 1u : 0u;
+            }
           }
 #pragma unroll
-          for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
-          const uint32_t nl = __popc(live);
-          for (uint32_t s = 0; s < nl; ++s) {
-            uint32_t jj = 0, pp = 0;
+          for (int sl = 0; sl < SL; ++sl) rk[sl] = key[sl] != ~0ull ? rk[sl] : 0xFFu;
 #pragma unroll
-            for (int j = 0; j < kRegDeg; ++j) {
-              jj = rk[j] == s ? (uint32_t)j : jj;
-              pp = rk[j] == s ? pk[j] : pp;
+          for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+          for (uint32_t s = 0; s < nlive; ++s) {
+            uint32_t jj = 0, pp = 0;
+            bool own = false;
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl) {
+              const bool m = rk[sl] == s;
+              own = own || m;
+              jj = m ? (uint32_t)sl * P + gl : jj;
+              pp = m ? pk[sl] : pp;
+            }
+            if (P > 1) {
+              const int src_lane = __ffs(__ballot_sync(gmask, own)) - 1;
+              jj = __shfl_sync(gmask, jj, src_lane);
+              pp = __shfl_sync(gmask, pp, src_lane);
             }
             step(b0 + jj, pp);
           }

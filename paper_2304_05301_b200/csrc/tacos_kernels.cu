@@ -77,10 +77,11 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   lay.off_inptr = s; s += al((N + 1u) * 4u, 16u);
   lay.smem_bytes = s;
   // threads: enough lanes for every destination row in one pass when possible
-  const uint32_t th_max = VPL > 1 ? 512u : 1024u;  // matches ThreadsFor<V> (__launch_bounds__)
+  const uint32_t th_max = VPL > 1 ? 512u : 768u;  // matches ThreadsFor<V> (__launch_bounds__)
   const uint32_t want = N * P > L / 2 ? N * P : L / 2;
   uint32_t th = 128;
   while (th < th_max && th < want) th <<= 1;
+  if (th > th_max) th = th_max;
   if (th < P) th = P;
   lay.threads = th;
   // Cluster size: split each job over Q CTAs (SMs) while the grid still fits on
