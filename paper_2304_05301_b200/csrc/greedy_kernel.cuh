@@ -107,9 +107,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   };
   // source version of NPU x (owned by CTA x / chunkN)
   auto hver_of = [&](uint32_t x) -> uint32_t {
-    const uint32_t o = x / chunkN;
-    if (o == crank) return hver[x];
-    return dsmem_ld(dsmem_addr(hver + x, o));
+    if (Q == 1 || x - d_lo < d_hi - d_lo) return hver[x];  // own NPU (the common case): no division
+    return dsmem_ld(dsmem_addr(hver + x, x / chunkN));
   };
 
   // ---- a2: state init (P:L89 precondition; P:L212 start at t = 0) ----
@@ -252,19 +251,19 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         // One step of the matching walk (a5) on in-link position p with pick draw pk.
         auto step = [&](uint32_t p, uint32_t pk) {
           const uint32_t sp = t_src[p];
-          const uint32_t owner = sp / chunkN;
+          const bool own_src = Q == 1 || sp - d_lo < d_hi - d_lo;
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
           uint4 cv[V];
           if (!ROWS_SMEM) {  // rows in HBM/L2, written by other SMs of the cluster: L2-coherent loads
             const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = __ldcg(&h4[v * P + gl]);
-          } else if (owner == crank) {
+          } else if (own_src) {
             const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
           } else {  // source row in a peer CTA's shared memory (DSMEM)
-            const uint32_t a = dsmem_addr(held + (size_t)sp * Wp, owner);
+            const uint32_t a = dsmem_addr(held + (size_t)sp * Wp, sp / chunkN);
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(v * P + gl) * 16u);
           }

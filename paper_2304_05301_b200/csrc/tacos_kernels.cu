@@ -272,39 +272,67 @@ __global__ void radix_hist_kernel(const unsigned long long *__restrict__ keys, u
   hist[(size_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
 }
 
-// exclusive scan of hist[0..total) in place, one block of 1024 threads
-__global__ void radix_scan_kernel(uint32_t *__restrict__ hist, uint32_t total) {
-  __shared__ uint32_t s_part[1024];
-  const uint32_t per = (total + 1023u) / 1024u;
-  const uint32_t b = threadIdx.x * per, en = min(b + per, total);
-  uint32_t sum = 0;
-  for (uint32_t i = b; i < en; ++i) sum += hist[i];
-  s_part[threadIdx.x] = sum;
+// Block-wide exclusive scan of one value per thread (blockDim = 256); returns
+// the exclusive prefix and writes the block total to *total.
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *s_warp, uint32_t *total) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
-  for (uint32_t o = 1; o < 1024; o <<= 1) {
-    uint32_t y = threadIdx.x >= o ? s_part[threadIdx.x - o] : 0u;
-    __syncthreads();
-    s_part[threadIdx.x] += y;
-    __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < 8 ? s_warp[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= (uint32_t)o) w += y;
+    }
+    if (lane < 8) s_warp[8 + lane] = w;
   }
-  uint32_t run = s_part[threadIdx.x] - sum;
-  for (uint32_t i = b; i < en; ++i) {
-    const uint32_t v = hist[i];
-    hist[i] = run;
-    run += v;
+  __syncthreads();
+  const uint32_t before = warp ? s_warp[8 + warp - 1] : 0u;
+  *total = s_warp[15];
+  __syncthreads();
+  return before + incl - v;
+}
+
+// One block per digit: exclusive scan of that digit's per-tile counts
+// hist[d][0..nb) in place (coalesced), digit total to totals[d].
+__global__ void radix_rowscan_kernel(uint32_t *__restrict__ hist, uint32_t nb, uint32_t *__restrict__ totals) {
+  __shared__ uint32_t s_warp[16];
+  uint32_t *row = hist + (size_t)blockIdx.x * nb;
+  uint32_t running = 0;
+  for (uint32_t base = 0; base < nb; base += 256u) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < nb ? row[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan256(v, s_warp, &tot);
+    if (i < nb) row[i] = running + ex;
+    running += tot;
   }
+  if (threadIdx.x == 0) totals[blockIdx.x] = running;
 }
 
 __global__ void radix_scatter_kernel(const unsigned long long *__restrict__ keys_in,
                                      const uint32_t *__restrict__ vals_in, uint64_t n, int shift,
-                                     const uint32_t *__restrict__ offs, uint32_t nblocks,
+                                     const uint32_t *__restrict__ offs, const uint32_t *__restrict__ totals,
+                                     uint32_t nblocks,
                                      unsigned long long *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
   constexpr int kWarps = kRsThreads / 32;
   __shared__ uint32_t s_off[256];
   __shared__ uint32_t s_wc[kWarps][256];
   __shared__ uint32_t s_tot[256];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  s_off[tid] = offs[(size_t)tid * nblocks + blockIdx.x];
+  {
+    __shared__ uint32_t s_warp[16];
+    uint32_t tot;
+    const uint32_t digit_base = block_excl_scan256(totals[tid], s_warp, &tot);
+    s_off[tid] = digit_base + offs[(size_t)tid * nblocks + blockIdx.x];
+  }
   const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
   for (int it = 0; it < kRsItems; ++it) {
     const uint64_t i = base + (uint64_t)it * kRsThreads + tid;
@@ -343,7 +371,7 @@ __global__ void radix_scatter_kernel(const unsigned long long *__restrict__ keys
 size_t rs_sort_scratch_bytes(uint64_t M) {
   const uint64_t nb = (M + kRsTile - 1) / kRsTile;
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  return al(M * 8) * 2 + al(M * 4) * 2 + al(nb * 256 * 4 + 4);
+  return al(M * 8) * 2 + al(M * 4) * 2 + al(nb * 256 * 4 + 256 * 4 + 4);
 }
 
 int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
@@ -362,6 +390,8 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
   uint32_t *va = reinterpret_cast<uint32_t *>(p); p += al(M * 4);
   uint32_t *vb = reinterpret_cast<uint32_t *>(p); p += al(M * 4);
   uint32_t *hist = reinterpret_cast<uint32_t *>(p);
+  const uint32_t nb0 = (uint32_t)((M + kRsTile - 1) / kRsTile);
+  uint32_t *totals = hist + (size_t)nb0 * 256u;
   uint32_t lbits = 1;
   while ((1ull << lbits) < (unsigned long long)L) ++lbits;
   uint32_t tbits = 1;
@@ -379,8 +409,8 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
   const uint32_t nb = (uint32_t)((M + kRsTile - 1) / kRsTile);
   for (uint32_t shift = 0; shift < bits; shift += 8) {
     radix_hist_kernel<<<nb, kRsThreads, 0, st>>>(ka, M, (int)shift, hist, nb);
-    radix_scan_kernel<<<1, 1024, 0, st>>>(hist, nb * 256u);
-    radix_scatter_kernel<<<nb, kRsThreads, 0, st>>>(ka, va, M, (int)shift, hist, nb, kb, vb);
+    radix_rowscan_kernel<<<256, 256, 0, st>>>(hist, nb, totals);
+    radix_scatter_kernel<<<nb, kRsThreads, 0, st>>>(ka, va, M, (int)shift, hist, totals, nb, kb, vb);
     nl += 3;
     rc = check_launch("radix pass");
     if (rc) return rc;
