@@ -255,7 +255,7 @@ __global__ void rs_emit_kernel(const uint32_t *__restrict__ vals, const Rec *__r
 
 // ---- LSD radix sort of (u64 key, u32 value), 8-bit digits, stable ----
 constexpr int kRsThreads = 256;
-constexpr int kRsItems = 16;
+constexpr int kRsItems = 4;
 constexpr int kRsTile = kRsThreads * kRsItems;
 
 __global__ void radix_hist_kernel(const unsigned long long *__restrict__ keys, uint64_t n, int shift,
