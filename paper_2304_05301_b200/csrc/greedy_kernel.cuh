@@ -220,19 +220,37 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     // Used when the destination groups leave threads idle (N*P < threads/2):
     // classification and Philox then run on all warps before PM.
     if (pre_draw) {
-      for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
-        unsigned char f = 0;
-        if (busy[q] <= t) {
-          f = 1;
-          if (seen[q] != hver_of(t_src[q])) {
-            const uint4 r = philox4x32_10(
-                make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
-            ord[q] = r.x;
-            pick[q] = r.y;
-            f = 2;
+      // kPB positions per thread per pass, Philox computed branch-free so the
+      // independent 10-round chains interleave (ILP)
+      constexpr int kPB = 4;
+      for (uint32_t base = p_lo + tid; base < p_hi; base += nthr * kPB) {
+        uint32_t lidv[kPB];
+        unsigned char f[kPB];
+#pragma unroll
+        for (int u = 0; u < kPB; ++u) {
+          const uint32_t q = base + (uint32_t)u * nthr;
+          f[u] = 0;
+          lidv[u] = 0;
+          if (q < p_hi) {
+            lidv[u] = t_lid[q];
+            if (busy[q] <= t) f[u] = seen[q] != hver_of(t_src[q]) ? 2 : 1;
           }
         }
-        lv[q] = f;
+        uint4 r[kPB];
+#pragma unroll
+        for (int u = 0; u < kPB; ++u)
+          r[u] = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), lidv[u], job.sigma), seed_lo, seed_hi);
+#pragma unroll
+        for (int u = 0; u < kPB; ++u) {
+          const uint32_t q = base + (uint32_t)u * nthr;
+          if (q < p_hi) {
+            lv[q] = f[u];
+            if (f[u] == 2) {
+              ord[q] = r[u].x;
+              pick[q] = r[u].y;
+            }
+          }
+        }
       }
       __syncthreads();
     }
@@ -249,11 +267,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         uint4 hv[V];
 
         // One step of the matching walk (a5) on in-link position p with pick draw pk.
-        auto step = [&](uint32_t p, uint32_t pk) {
+        // held[src] row of in-link p into registers (own shared memory, a peer's via DSMEM, or L2)
+        auto load_row = [&](uint32_t p, uint4 (&cv)[V]) {
           const uint32_t sp = t_src[p];
           const bool own_src = Q == 1 || sp - d_lo < d_hi - d_lo;
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
-          uint4 cv[V];
           if (!ROWS_SMEM) {  // rows in HBM/L2, written by other SMs of the cluster: L2-coherent loads
             const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
 #pragma unroll
@@ -267,6 +285,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(v * P + gl) * 16u);
           }
+        };
+        // One step of the matching walk (a5) on in-link p, pick draw pk, loaded row cv.
+        auto step_row = [&](uint32_t p, uint32_t pk, uint4 (&cv)[V]) {
           uint32_t incl[V], tot[V];
           uint32_t K = 0;
 #pragma unroll
@@ -283,7 +304,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             K += tot[v];
           }
           if (K == 0u) {
-            if (gl == 0) seen[p] = hver_of(sp);
+            if (gl == 0) seen[p] = hver_of(t_src[p]);
             return;
           }
           const uint32_t r = __umulhi(pk, K);  // floor(u_pick * K / 2^32)
@@ -335,6 +356,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             const uint32_t lid = t_lid[p];
             atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
           }
+        };
+
+        auto step = [&](uint32_t p, uint32_t pk) {
+          uint4 cv[V];
+          load_row(p, cv);
+          step_row(p, pk, cv);
         };
 
         if (P <= 8 && deg <= (uint32_t)kRegDeg) {
@@ -407,8 +434,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (int sl = 0; sl < SL; ++sl) rk[sl] = key[sl] != ~0ull ? rk[sl] : 0xFFu;
 #pragma unroll
           for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
-          for (uint32_t s = 0; s < nlive; ++s) {
-            uint32_t jj = 0, pp = 0;
+          // walk order: in-link of rank s (owning lane broadcasts position and pick draw)
+          auto link_of_rank = [&](uint32_t s, uint32_t &jj, uint32_t &pp) {
+            jj = 0;
+            pp = 0;
             bool own = false;
 #pragma unroll
             for (int sl = 0; sl < SL; ++sl) {
@@ -422,7 +451,25 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               jj = __shfl_sync(gmask, jj, src_lane);
               pp = __shfl_sync(gmask, pp, src_lane);
             }
-            step(b0 + jj, pp);
+          };
+          // software pipeline: the next in-link's row is loaded before the current step
+          // (rows do not change during PM; only `have` does, and it is applied in step_row)
+          uint32_t jj, pp;
+          link_of_rank(0, jj, pp);
+          uint4 row[V];
+          load_row(b0 + jj, row);
+          for (uint32_t s = 0; s < nlive; ++s) {
+            uint32_t jn = 0, pn = 0;
+            uint4 nrow[V];
+            if (s + 1 < nlive) {
+              link_of_rank(s + 1, jn, pn);
+              load_row(b0 + jn, nrow);
+            }
+            step_row(b0 + jj, pp, row);
+            jj = jn;
+            pp = pn;
+#pragma unroll
+            for (int v = 0; v < V; ++v) row[v] = nrow[v];
           }
 #pragma unroll
           for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];
