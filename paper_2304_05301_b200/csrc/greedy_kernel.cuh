@@ -61,6 +61,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const Job job = jobs[blockIdx.x / Q];
   const DevTopo T = *job.topo;
   const uint32_t N = T.N, L = T.L, Wp = T.Wp;
+  // row stride in words: padded in shared memory so rows of different NPUs start in different
+  // bank groups (a warp's 128-bit loads of random rows would otherwise 16-way conflict)
+  const uint32_t Wr = ROWS_SMEM ? lay.row_stride : Wp;
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
   const uint32_t *__restrict__ p_src = T.p_src;
   const uint32_t *__restrict__ p_w = T.p_w;
@@ -71,7 +74,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *held;
   if constexpr (ROWS_SMEM) held = reinterpret_cast<uint32_t *>(smem);
   else held = job.g_rows;
-  uint32_t *have = held + (size_t)N * Wp;  // held | pending | claimed (R4)
+  uint32_t *have = held + (size_t)N * Wr;  // held | pending | claimed (R4)
   unsigned char *links_base;
   if constexpr (LINKS_SMEM) links_base = smem + (ROWS_SMEM ? lay.rows_bytes : 0u);
   else links_base = job.g_links;
@@ -115,17 +118,17 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t NW = N * Wp;
   for (uint32_t i = d_lo * Wp + tid; i < d_hi * Wp; i += nthr) {
     uint32_t v;
+    const uint32_t x = i / Wp, q = i - x * Wp;
     if (custom) {
       v = __ldg(&T.pre[i]);
     } else {  // AG: chunks x*k .. x*k+k-1 (R12)
-      const uint32_t x = i / Wp, q = i - x * Wp;
       const uint32_t lo = x * T.k, hi = lo + T.k, wlo = q * 32u, whi = wlo + 32u;
       const uint32_t a = lo > wlo ? lo : wlo, b = hi < whi ? hi : whi;
       v = 0u;
       if (a < b) v = ((b - a) == 32u ? 0xFFFFFFFFu : ((1u << (b - a)) - 1u)) << (a - wlo);
     }
-    held[i] = v;
-    have[i] = v;
+    held[(size_t)x * Wr + q] = v;
+    have[(size_t)x * Wr + q] = v;
   }
   for (uint32_t p = p_lo + tid; p < p_hi; p += nthr) {
     busy[p] = 0ull;
@@ -189,7 +192,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             rec[idx] = r;
           }
           if (b == t) {  // R7: held by dst from this instant
-            held[(size_t)d * Wp + (c >> 5)] |= 1u << (c & 31u);
+            held[(size_t)d * Wr + (c >> 5)] |= 1u << (c & 31u);
             cur[p] = kNone;
             got = true;
             ++arr;
@@ -262,7 +265,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       for (uint32_t d = d_lo + tid / P; d < d_hi; d += ngroups) {
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         const uint32_t deg = b1 - b0;
-        uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wp);
+        uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
         const uint4 *post4 = reinterpret_cast<const uint4 *>(T.post + (size_t)d * Wp);
         uint4 hv[V];
 
@@ -273,15 +276,15 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           const bool own_src = Q == 1 || sp - d_lo < d_hi - d_lo;
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
           if (!ROWS_SMEM) {  // rows in HBM/L2, written by other SMs of the cluster: L2-coherent loads
-            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
+            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = __ldcg(&h4[v * P + gl]);
           } else if (own_src) {
-            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wp);
+            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
           } else {  // source row in a peer CTA's shared memory (DSMEM)
-            const uint32_t a = dsmem_addr(held + (size_t)sp * Wp, sp / chunkN);
+            const uint32_t a = dsmem_addr(held + (size_t)sp * Wr, sp / chunkN);
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(v * P + gl) * 16u);
           }

@@ -61,7 +61,8 @@ struct JobOut {
 // Byte offsets of the per-block arrays, either in dynamic shared memory or in
 // the job's global scratch (rows / links regions).
 struct Layout {
-  uint32_t rows_bytes;   // 2*N*Wp*4 (held then have)
+  uint32_t rows_bytes;   // 2*N*row_stride*4 (held then have)
+  uint32_t row_stride;   // words between consecutive rows in shared memory (Wp, padded)
   uint32_t links_bytes;  // per-position arrays
   // within the links region
   uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv;

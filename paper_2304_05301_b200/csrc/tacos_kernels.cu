@@ -42,7 +42,10 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
                    uint32_t n_sms) {
   auto al = [](uint32_t x, uint32_t a) { return (x + a - 1u) / a * a; };
   Layout lay{};
-  lay.rows_bytes = al(2u * N * Wp * 4u, 16u);
+  // pad the shared-memory row stride by one 16-byte vector when the row is an even
+  // number of vectors: consecutive rows then start 4 banks apart
+  lay.row_stride = ((Wp / 4u) % 2u == 0u) ? Wp + 4u : Wp;
+  lay.rows_bytes = al(2u * N * lay.row_stride * 4u, 16u);
   uint32_t o = 0;
   lay.off_busy = o; o += al(L * 8u, 16u);
   lay.off_cur = o; o += al(L * 4u, 16u);
