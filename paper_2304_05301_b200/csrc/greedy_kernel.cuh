@@ -48,6 +48,9 @@ template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM>
 __global__ void __launch_bounds__(ThreadsFor<V>::value, 1)
 greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Layout lay) {
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
+  // one thread per destination with shared-memory rows: `have` stays in shared memory and a
+  // claim is one word update (no per-word predicated register updates)
+  constexpr bool kHaveSmem = (P == 1) && ROWS_SMEM;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_min, s_delivered, s_V, s_D, s_M;
   // cluster exchange slots, indexed by the writer's rank (plain remote stores, no 64-bit DSMEM atomics)
@@ -295,7 +298,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           uint32_t K = 0;
 #pragma unroll
           for (int v = 0; v < V; ++v) {
-            cv[v] = andnot4(cv[v], hv[v]);  // held[src] & ~have[d]
+            if constexpr (kHaveSmem) cv[v] = andnot4(cv[v], have4[v * P + gl]);  // held[src] & ~have[d]
+            else cv[v] = andnot4(cv[v], hv[v]);
             if (custom) cv[v] = and4(cv[v], __ldg(&post4[v * P + gl]));  // & post[d]
             incl[v] = popc4(cv[v]);
 #pragma unroll
@@ -341,13 +345,18 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           rr = m ? rr - cz : rr; wi = m ? 3u : wi; word = m ? x.w : word;
           const uint32_t bit = select_bit(word, rr);
           const uint32_t mask = mine ? (1u << bit) : 0u;
+          // claim: withheld from d's other in-links (R4)
+          if constexpr (kHaveSmem) {
+            reinterpret_cast<uint32_t *>(have4)[(uint32_t)vsel * 4u + wi] |= mask;  // one word, dynamic index
+          } else {
 #pragma unroll
-          for (int v = 0; v < V; ++v) {  // claim: withheld from d's other in-links (R4)
-            if (vsel == v) {
-              hv[v].x |= wi == 0u ? mask : 0u;
-              hv[v].y |= wi == 1u ? mask : 0u;
-              hv[v].z |= wi == 2u ? mask : 0u;
-              hv[v].w |= wi == 3u ? mask : 0u;
+            for (int v = 0; v < V; ++v) {
+              if (vsel == v) {
+                hv[v].x |= wi == 0u ? mask : 0u;
+                hv[v].y |= wi == 1u ? mask : 0u;
+                hv[v].z |= wi == 2u ? mask : 0u;
+                hv[v].w |= wi == 3u ? mask : 0u;
+              }
             }
           }
           uint32_t chunk = (((uint32_t)vsel * P + gl) * 4u + wi) * 32u + bit;
@@ -436,7 +445,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
           for (int sl = 0; sl < SL; ++sl) rk[sl] = key[sl] != ~0ull ? rk[sl] : 0xFFu;
 #pragma unroll
-          for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+          for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v * P + gl];
           // walk order: in-link of rank s (owning lane broadcasts position and pick draw)
           auto link_of_rank = [&](uint32_t s, uint32_t &jj, uint32_t &pp) {
             jj = 0;
@@ -475,7 +484,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             for (int v = 0; v < V; ++v) row[v] = nrow[v];
           }
 #pragma unroll
-          for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];
+          for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v * P + gl] = hv[v];
           continue;
         }
 
@@ -528,13 +537,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         }
         if (P > 1) __syncwarp(gmask);
 #pragma unroll
-        for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+        for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v * P + gl];
         for (uint32_t s = 0; s < nl; ++s) {
           const uint32_t p = order[b0 + s];
           step(p, pick[p]);
         }
 #pragma unroll
-        for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];
+        for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v * P + gl] = hv[v];
       }
     }
     if (tracing) ts[4] = clock64();
