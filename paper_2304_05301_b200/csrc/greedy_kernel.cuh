@@ -7,6 +7,7 @@
 //   PA  (per destination)    records of the previous event in link-id order;
 //                            arrivals at t: held[dst] |= chunk (R7)
 //       -- barrier --        done test: delivered == required
+//                            (optionally the Philox draws run on PA's spare threads)
 //   PM  (per destination,    free in-links (busy_until <= t); exact skip of a
 //        P lanes each)       link whose source is unchanged since its last
 //                            empty visit; Philox draws (R2); shorter-link-first
@@ -165,6 +166,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t gmask = (P == 32) ? 0xFFFFFFFFu : (((1u << P) - 1u) << (lane & ~(uint32_t)(P - 1)));
   const uint32_t ngroups = nthr / P;
   const bool pre_draw = lay.pre_draw != 0u;
+  // PA: threads [0, nA) handle destinations; with pre_draw the others draw Philox values
+  const uint32_t nA = pre_draw ? max(32u, min(nthr / 2u, ((d_hi - d_lo) + 31u) & ~31u)) : nthr;
   const bool tracing = job.trace != nullptr && tid == 0;
 
   for (;;) {
@@ -176,8 +179,34 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       const uint32_t *bm_prev = bitmap2 + ((e + 1u) & 1u) * nbw;  // bitmap of event e-1
       uint32_t arr = 0;
       // one thread per destination: its in-links are contiguous positions, so the
-      // held row is updated without atomics
-      for (uint32_t d = d_lo + tid; d < d_hi; d += nthr) {
+      // held row is updated without atomics.  With pre_draw, threads [nA, nthr)
+      // draw the Philox values of every link free at t meanwhile (t and busy_until
+      // are fixed here; liveness is decided in PM after the arrivals).
+      if (tid >= nA) {
+        constexpr int kPB = 4;  // positions per pass: branch-free Philox chains interleave (ILP)
+        const uint32_t nD = nthr - nA;
+        for (uint32_t base = p_lo + (tid - nA); base < p_hi; base += nD * kPB) {
+          uint32_t lidv[kPB];
+#pragma unroll
+          for (int u = 0; u < kPB; ++u) {
+            const uint32_t q = base + (uint32_t)u * nD;
+            lidv[u] = q < p_hi ? t_lid[q] : 0u;
+          }
+          uint4 r[kPB];
+#pragma unroll
+          for (int u = 0; u < kPB; ++u)
+            r[u] = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), lidv[u], job.sigma), seed_lo, seed_hi);
+#pragma unroll
+          for (int u = 0; u < kPB; ++u) {
+            const uint32_t q = base + (uint32_t)u * nD;
+            if (q < p_hi && busy[q] <= t) {
+              ord[q] = r[u].x;
+              pick[q] = r[u].y;
+            }
+          }
+        }
+      }
+      for (uint32_t d = d_lo + tid; d < d_hi && tid < nA; d += nA) {
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         bool got = false;
         for (uint32_t p = b0; p < b1; ++p) {
@@ -222,44 +251,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     if (tid == 0) s_rec_base = s_next_base;
     ++E;
 
-    // ================= PB (optional): per-position draws by every thread =================
-    // Used when the destination groups leave threads idle (N*P < threads/2):
-    // classification and Philox then run on all warps before PM.
-    if (pre_draw) {
-      // kPB positions per thread per pass, Philox computed branch-free so the
-      // independent 10-round chains interleave (ILP)
-      constexpr int kPB = 4;
-      for (uint32_t base = p_lo + tid; base < p_hi; base += nthr * kPB) {
-        uint32_t lidv[kPB];
-        unsigned char f[kPB];
-#pragma unroll
-        for (int u = 0; u < kPB; ++u) {
-          const uint32_t q = base + (uint32_t)u * nthr;
-          f[u] = 0;
-          lidv[u] = 0;
-          if (q < p_hi) {
-            lidv[u] = t_lid[q];
-            if (busy[q] <= t) f[u] = seen[q] != hver_of(t_src[q]) ? 2 : 1;
-          }
-        }
-        uint4 r[kPB];
-#pragma unroll
-        for (int u = 0; u < kPB; ++u)
-          r[u] = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), lidv[u], job.sigma), seed_lo, seed_hi);
-#pragma unroll
-        for (int u = 0; u < kPB; ++u) {
-          const uint32_t q = base + (uint32_t)u * nthr;
-          if (q < p_hi) {
-            lv[q] = f[u];
-            if (f[u] == 2) {
-              ord[q] = r[u].x;
-              pick[q] = r[u].y;
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
     if (tracing) ts[3] = clock64();
 
     // ================= PM: per-destination draws, order and matching =================
@@ -392,10 +383,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               const uint32_t q = b0 + j;
               bool isfree, islive;
               uint32_t o = 0;
-              if (pre_draw) {
-                const unsigned char f = lv[q];
-                isfree = f != 0;
-                islive = f == 2;
+              if (pre_draw) {  // draws made in PA; liveness needs the arrivals of PA
+                isfree = busy[q] <= t;
+                islive = isfree && seen[q] != hver_of(t_src[q]);
                 if (islive) {
                   o = ord[q];
                   pk[sl] = pick[q];
@@ -464,24 +454,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               pp = __shfl_sync(gmask, pp, src_lane);
             }
           };
-          // software pipeline: the next in-link's row is loaded before the current step
-          // (rows do not change during PM; only `have` does, and it is applied in step_row)
-          uint32_t jj, pp;
-          link_of_rank(0, jj, pp);
-          uint4 row[V];
-          load_row(b0 + jj, row);
           for (uint32_t s = 0; s < nlive; ++s) {
-            uint32_t jn = 0, pn = 0;
-            uint4 nrow[V];
-            if (s + 1 < nlive) {
-              link_of_rank(s + 1, jn, pn);
-              load_row(b0 + jn, nrow);
-            }
-            step_row(b0 + jj, pp, row);
-            jj = jn;
-            pp = pn;
-#pragma unroll
-            for (int v = 0; v < V; ++v) row[v] = nrow[v];
+            uint32_t jj, pp;
+            link_of_rank(s, jj, pp);
+            step(b0 + jj, pp);
           }
 #pragma unroll
           for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v * P + gl] = hv[v];
@@ -492,8 +468,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         uint32_t nfree = 0, nl = 0;
         for (uint32_t q = b0 + gl; q < b1; q += P) {
           unsigned char f;
-          if (pre_draw) {
-            f = lv[q];
+          if (pre_draw) {  // draws made in PA
+            f = busy[q] <= t ? (seen[q] != hver_of(t_src[q]) ? 2 : 1) : 0;
+            lv[q] = f;
           } else {
             f = 0;
             if (busy[q] <= t) {  // free: nothing in flight on it
