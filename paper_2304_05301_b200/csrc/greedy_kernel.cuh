@@ -209,9 +209,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       for (uint32_t d = d_lo + tid; d < d_hi && tid < nA; d += nA) {
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         bool got = false;
-        auto visit = [&](uint32_t p, uint32_t c, unsigned long long b, uint32_t w, uint32_t lid) {
-          if (c == kNone) return;
-          if (rec != nullptr && e > 0u && b - w == t_prev) {
+        for (uint32_t p = b0; p < b1; ++p) {
+          const uint32_t c = cur[p];
+          if (c == kNone) continue;
+          const unsigned long long b = busy[p];
+          if (rec != nullptr && e > 0u && b - t_w[p] == t_prev) {
+            const uint32_t lid = t_lid[p];
             const uint32_t wi = lid >> 5;
             const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
             Rec r;
@@ -226,25 +229,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             got = true;
             ++arr;
           }
-        };
-        if (b1 - b0 <= (uint32_t)kRegDeg) {  // loads of all in-links first (ILP), then the updates
-          uint32_t cc[kRegDeg], ww[kRegDeg], ll[kRegDeg];
-          unsigned long long bb[kRegDeg];
-#pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) {
-            const uint32_t p = b0 + j;
-            cc[j] = kNone;
-            if (p < b1) {
-              cc[j] = cur[p];
-              bb[j] = busy[p];
-              ww[j] = t_w[p];
-              ll[j] = t_lid[p];
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) visit(b0 + j, cc[j], bb[j], ww[j], ll[j]);
-        } else {
-          for (uint32_t p = b0; p < b1; ++p) visit(p, cur[p], busy[p], t_w[p], t_lid[p]);
         }
         if (got) hver[d] = e;
       }
