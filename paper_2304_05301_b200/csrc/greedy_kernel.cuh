@@ -45,7 +45,7 @@ struct ThreadsFor {
   static constexpr int value = V > 1 ? 512 : 768;  // registers: <= 128 resp. <= 85 per thread
 };
 
-template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM>
+template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM, bool REG_PATH>
 __global__ void __launch_bounds__(ThreadsFor<V>::value, 1)
 greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Layout lay) {
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
@@ -367,7 +367,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           step_row(p, pk, cv);
         };
 
-        if (P <= 8 && deg <= (uint32_t)kRegDeg) {
+        // REG_PATH (every in-degree <= kRegDeg, P <= 8): ranks in registers; else shared memory
+        if constexpr (REG_PATH && P <= 8) {
           // ---- register path: the group owns the destination's <= kRegDeg in-links, in-link j
           //      in slot j / P of lane j % P; ranks and the walk order stay in registers ----
           constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
@@ -461,9 +462,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
 #pragma unroll
           for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v * P + gl] = hv[v];
-          continue;
-        }
-
+        } else {
         // ---- shared-memory path: per-position draws, ranks and order ----
         uint32_t nfree = 0, nl = 0;
         for (uint32_t q = b0 + gl; q < b1; q += P) {
@@ -521,6 +520,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v * P + gl] = hv[v];
+        }
       }
     }
     if (tracing) ts[4] = clock64();
@@ -641,9 +641,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   }
 }
 
-template <int P, int V, bool R, bool K>
+template <int P, int V, bool R, bool K, bool G>
 int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
-  auto fn = greedy_kernel<P, V, R, K>;
+  auto fn = greedy_kernel<P, V, R, K, G>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.smem_bytes);
   if (e != cudaSuccess) {
     snprintf(cuda_error_buffer(), 256, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -677,9 +677,14 @@ int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, Job
 
 template <int P, int V>
 int launch_greedy_pv(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
-  if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true>(lay, d_jobs, n_jobs, d_outs, st);
-  if (lay.links_in_smem) return launch_greedy_one<P, V, false, true>(lay, d_jobs, n_jobs, d_outs, st);
-  return launch_greedy_one<P, V, false, false>(lay, d_jobs, n_jobs, d_outs, st);
+  if (lay.reg_path && P <= 8) {
+    if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true, true>(lay, d_jobs, n_jobs, d_outs, st);
+    if (lay.links_in_smem) return launch_greedy_one<P, V, false, true, true>(lay, d_jobs, n_jobs, d_outs, st);
+    return launch_greedy_one<P, V, false, false, true>(lay, d_jobs, n_jobs, d_outs, st);
+  }
+  if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true, false>(lay, d_jobs, n_jobs, d_outs, st);
+  if (lay.links_in_smem) return launch_greedy_one<P, V, false, true, false>(lay, d_jobs, n_jobs, d_outs, st);
+  return launch_greedy_one<P, V, false, false, false>(lay, d_jobs, n_jobs, d_outs, st);
 }
 
 // One translation unit per P (greedy_p<P>.cu) instantiates these.

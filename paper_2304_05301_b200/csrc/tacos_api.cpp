@@ -513,6 +513,14 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     g.P = P0;
     g.VPL = V0;
     g.lay = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, n_jobs - begin, (uint32_t)n_sms);
+    uint32_t max_deg = 0;
+    for (size_t gk = gi; gk < gj; ++gk) {
+      const tacos_topology *tt = pl->parts[order[gk]].topo;
+      for (int o = 0; o < 2; ++o)
+        for (int32_t d = 0; d < tt->N; ++d) max_deg = std::max(max_deg, tt->in_ptr[o][d + 1] - tt->in_ptr[o][d]);
+    }
+    g.lay.reg_path = max_deg <= 8u ? 1u : 0u;
+    if (const char *env = getenv("TACOS_REG_PATH")) g.lay.reg_path = (uint32_t)atoi(env);
     g.job_begin = begin;
     g.job_end = n_jobs;
     pl->groups.push_back(g);

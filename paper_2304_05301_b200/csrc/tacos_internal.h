@@ -22,6 +22,7 @@ struct DevTopo {
   uint32_t Wp;       // padded words per row = 4 * P * VPL
   uint32_t P, VPL;   // lanes per destination, uint4 vectors per lane
   uint32_t custom;   // 1: pre/post rows given
+  uint32_t max_deg;  // maximum in-degree
   uint64_t required; // deliveries needed
   const uint32_t *in_ptr; // [N+1]
   const uint32_t *p_src;  // [L] source NPU of position p
@@ -74,6 +75,7 @@ struct Layout {
   uint32_t threads;
   uint32_t pre_draw;     // 1: draws per position by all threads before the destination phase
   uint32_t cluster;      // CTAs per job (thread-block cluster size), 1 = one CTA per job
+  uint32_t reg_path;     // 1: every in-degree <= 8 (register ranking path)
 };
 
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,
