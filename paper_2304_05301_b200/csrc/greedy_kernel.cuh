@@ -367,8 +367,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           step_row(p, pk, cv);
         };
 
-        // REG_PATH (every in-degree <= kRegDeg, P <= 8): ranks in registers; else shared memory
-        if constexpr (REG_PATH && P <= 8) {
+        // REG_PATH (every in-degree <= kRegDeg): ranks in registers; else shared memory
+        if constexpr (REG_PATH) {
           // ---- register path: the group owns the destination's <= kRegDeg in-links, in-link j
           //      in slot j / P of lane j % P; ranks and the walk order stay in registers ----
           constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
@@ -677,7 +677,7 @@ int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, Job
 
 template <int P, int V>
 int launch_greedy_pv(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
-  if (lay.reg_path && P <= 8) {
+  if (lay.reg_path) {
     if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true, true>(lay, d_jobs, n_jobs, d_outs, st);
     if (lay.links_in_smem) return launch_greedy_one<P, V, false, true, true>(lay, d_jobs, n_jobs, d_outs, st);
     return launch_greedy_one<P, V, false, false, true>(lay, d_jobs, n_jobs, d_outs, st);
