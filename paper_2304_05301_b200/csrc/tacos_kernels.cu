@@ -90,7 +90,7 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   // Cluster size: split each job over Q CTAs (SMs) while the grid still fits on
   // the chip and every CTA keeps >= 32 destinations.
   uint32_t Q = 1;
-  while (Q < 8 && (uint64_t)n_jobs * Q * 2 <= n_sms && N / (Q * 2) >= 32) Q <<= 1;
+  while (Q < 4 && (uint64_t)n_jobs * Q * 2 <= n_sms && N / (Q * 2) >= 32) Q <<= 1;  // Q = 8 measured slower (barriers)
   if (const char *env = getenv("TACOS_CLUSTER")) {
     const uint32_t want = (uint32_t)atoi(env);
     if (want >= 1 && want <= 8 && (want & (want - 1)) == 0) Q = want;
