@@ -267,6 +267,50 @@ int tacos_eval(const tacos_topology *topo, const tacos_synth_params *p, const ta
                tacos_eval_report *out);
 
 /* ---------------------------------------------------------------------- */
+/* Topology front-end (host)                             */
+/* ---------------------------------------------------------------------- */
+
+/* One dimension of a hierarchical topology ("3D topology of
+ * Ring_FullyConnected_Switch"; SPEC S:L84-91 composition).
+ *   TACOS_DIM_RING:   i -> i+1 (mod n); bidirectional adds i -> i-1 (a 2-node
+ *                     ring has one link per direction)
+ *   TACOS_DIM_FC:     every ordered pair
+ *   TACOS_DIM_SWITCH: switch unwound with degree d (§IV.D):
+ *                     i -> i+1 .. i+d (mod n), each link bw / d (bw must be a
+ *                     multiple of d); d = 1 with `bidirectional` is the paper's
+ *                     bi-directional ring variation at full bandwidth
+ *   TACOS_DIM_PATH:   1-D mesh, i -> i+1 and i -> i-1 where they exist
+ * Every link of a dimension gets that dimension's alpha and bandwidth. */
+enum { TACOS_DIM_RING = 0, TACOS_DIM_FC = 1, TACOS_DIM_SWITCH = 2, TACOS_DIM_PATH = 3 };
+typedef struct {
+  int32_t kind;
+  uint32_t n;             /* NPUs along this dimension (>= 2) */
+  uint32_t degree;        /* SWITCH only: 1 <= d <= n - 1 */
+  uint32_t bidirectional; /* RING / SWITCH with d = 1 */
+  uint32_t alpha_ns;
+  uint32_t bw;            /* bytes per ns (total per NPU for SWITCH) */
+} tacos_dim_spec;
+
+/* Product of the dimensions: NPU id = c_0 + n_0 (c_1 + n_1 (c_2 + ...)) (dimension
+ * 0 fastest).  Links in canonical order: NPU by NPU, then dimension by dimension,
+ * then the dimension's own link order from c_i.  Writes up to `capacity` links to
+ * src/dst/alpha/bw (caller host memory) and the counts to *n_npus / *n_links;
+ * call with capacity 0 (arrays may be NULL) to get the sizes.
+ * Errors: TACOS_E_INVALID_ARG (bad spec, N >= 2^31), TACOS_E_CAPACITY. */
+int tacos_build_hierarchical(const tacos_dim_spec *dims, uint32_t n_dims, int32_t *n_npus, int32_t *n_links,
+                             int32_t *src, int32_t *dst, uint32_t *alpha_ns, uint32_t *bw, int64_t capacity);
+
+/* Remove NPUs (and every link touching them), renumbering the remaining NPUs
+ * densely in ascending order and keeping the relative link order (PAPER
+ * P:L406, Table IV: a mesh with failed NPUs is re-synthesized on the
+ * reduced topology).  Outputs as tacos_build_hierarchical; `old_id` (may be
+ * NULL, capacity >= N - n_removed) receives the original id of each new NPU. */
+int tacos_remove_npus(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst, const uint32_t *alpha_ns,
+                      const uint32_t *bw, const int32_t *removed, uint32_t n_removed, int32_t *out_n_npus,
+                      int32_t *out_n_links, int32_t *out_src, int32_t *out_dst, uint32_t *out_alpha, uint32_t *out_bw,
+                      int64_t capacity, int32_t *old_id);
+
+/* ---------------------------------------------------------------------- */
 /* Misc                                                                    */
 /* ---------------------------------------------------------------------- */
 const char *tacos_strerror(int code);

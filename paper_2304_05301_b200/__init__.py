@@ -83,6 +83,15 @@ class tacos_winner(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
 
 
+class tacos_dim_spec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("n", ctypes.c_uint32), ("degree", ctypes.c_uint32),
+                ("bidirectional", ctypes.c_uint32), ("alpha_ns", ctypes.c_uint32), ("bw", ctypes.c_uint32)]
+
+
+TACOS_DIM_RING, TACOS_DIM_FC, TACOS_DIM_SWITCH, TACOS_DIM_PATH = 0, 1, 2, 3
+DIM_KINDS = {"ring": TACOS_DIM_RING, "fc": TACOS_DIM_FC, "switch": TACOS_DIM_SWITCH, "path": TACOS_DIM_PATH}
+
+
 class tacos_eval_report(ctypes.Structure):
     _fields_ = [("T", ctypes.c_uint64), ("T_rs", ctypes.c_uint64), ("n_violations", ctypes.c_uint64),
                 ("per_kind", ctypes.c_uint64 * 7), ("first_kind", ctypes.c_int32), ("reserved", ctypes.c_uint32),
@@ -128,6 +137,11 @@ SIGNATURES = {
     "tacos_plan_stats": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_result), _VP]),
     "tacos_eval": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_synth_params), _VP, ctypes.c_uint64,
                                   ctypes.POINTER(tacos_eval_report)]),
+    "tacos_build_hierarchical": (ctypes.c_int, [ctypes.POINTER(tacos_dim_spec), ctypes.c_uint32, _I32P, _I32P, _I32P,
+                                                _I32P, _U32P, _U32P, ctypes.c_int64]),
+    "tacos_remove_npus": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _I32P, _I32P, _U32P, _U32P, _I32P,
+                                         ctypes.c_uint32, _I32P, _I32P, _I32P, _I32P, _U32P, _U32P, ctypes.c_int64,
+                                         _I32P]),
     "tacos_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "tacos_last_error": (ctypes.c_char_p, []),
     "tacos_abi_version": (ctypes.c_int, []),
@@ -464,3 +478,57 @@ class Plan:
 
 def sends_from_bytes(buf: np.ndarray) -> np.ndarray:
     return np.frombuffer(np.ascontiguousarray(buf).tobytes(), dtype=SEND_DTYPE)
+
+
+# --------------------------------------------------------------------------
+# topology front-end (f4)
+# --------------------------------------------------------------------------
+def tacos_build_hierarchical(dims):
+    """dims: list of dicts {kind: ring|fc|switch|path, n, degree=1, bidirectional=0,
+    alpha_ns, bw}.  Returns (n_npus, src, dst, alpha_ns, bw) numpy arrays."""
+    lib = load_library()
+    arr = (tacos_dim_spec * len(dims))()
+    for a, d in zip(arr, dims):
+        a.kind = DIM_KINDS[d["kind"]] if isinstance(d["kind"], str) else int(d["kind"])
+        a.n = d["n"]
+        a.degree = d.get("degree", 1)
+        a.bidirectional = int(d.get("bidirectional", 0))
+        a.alpha_ns = d.get("alpha_ns", 500)
+        a.bw = d["bw"]
+    n = ctypes.c_int32()
+    m = ctypes.c_int32()
+    _check(lib.tacos_build_hierarchical(arr, len(dims), ctypes.byref(n), ctypes.byref(m), None, None, None, None, 0),
+           "tacos_build_hierarchical")
+    L = m.value
+    src = np.zeros(L, np.int32)
+    dst = np.zeros(L, np.int32)
+    al = np.zeros(L, np.uint32)
+    bw = np.zeros(L, np.uint32)
+    _check(lib.tacos_build_hierarchical(arr, len(dims), ctypes.byref(n), ctypes.byref(m), _ptr(src, ctypes.c_int32),
+                                        _ptr(dst, ctypes.c_int32), _ptr(al, ctypes.c_uint32), _ptr(bw, ctypes.c_uint32),
+                                        L), "tacos_build_hierarchical")
+    return n.value, src, dst, al, bw
+
+
+def tacos_remove_npus(n_npus, src, dst, alpha_ns, bw, removed):
+    lib = load_library()
+    s_ = np.ascontiguousarray(src, np.int32)
+    d_ = np.ascontiguousarray(dst, np.int32)
+    a_ = _u32(alpha_ns)
+    b_ = _u32(bw)
+    r_ = np.ascontiguousarray(removed, np.int32)
+    L = s_.shape[0]
+    n2 = ctypes.c_int32()
+    m2 = ctypes.c_int32()
+    os_ = np.zeros(max(L, 1), np.int32)
+    od_ = np.zeros(max(L, 1), np.int32)
+    oa_ = np.zeros(max(L, 1), np.uint32)
+    ob_ = np.zeros(max(L, 1), np.uint32)
+    oid = np.zeros(max(n_npus, 1), np.int32)
+    _check(lib.tacos_remove_npus(n_npus, L, _ptr(s_, ctypes.c_int32), _ptr(d_, ctypes.c_int32), _ptr(a_, ctypes.c_uint32),
+                                 _ptr(b_, ctypes.c_uint32), _ptr(r_, ctypes.c_int32), r_.shape[0], ctypes.byref(n2),
+                                 ctypes.byref(m2), _ptr(os_, ctypes.c_int32), _ptr(od_, ctypes.c_int32),
+                                 _ptr(oa_, ctypes.c_uint32), _ptr(ob_, ctypes.c_uint32), max(L, n_npus),
+                                 _ptr(oid, ctypes.c_int32)), "tacos_remove_npus")
+    k = m2.value
+    return n2.value, os_[:k].copy(), od_[:k].copy(), oa_[:k].copy(), ob_[:k].copy(), oid[:n2.value].copy()

@@ -1202,3 +1202,156 @@ extern "C" int tacos_philox_device(const uint32_t ctr[4], const uint32_t key[2],
   cudaFree(d);
   return rc;
 }
+
+// ---------------------------------------------------------------------------
+// Topology front-end (f4): hierarchical products of dimensions with switch
+// unwinding (§IV.D), NPU removal.
+// ---------------------------------------------------------------------------
+namespace {
+struct DimLink {
+  uint32_t a, b, alpha, bw;
+};
+
+int dim_links(const tacos_dim_spec &d, std::vector<DimLink> &out) {
+  out.clear();
+  const uint32_t n = d.n;
+  if (n < 2) return fail(TACOS_E_INVALID_ARG, "dimension of size %u < 2", n);
+  if (d.bw == 0) return fail(TACOS_E_INVALID_ARG, "dimension bandwidth 0");
+  switch (d.kind) {
+    case TACOS_DIM_RING:
+      for (uint32_t i = 0; i < n; ++i) {
+        out.push_back({i, (i + 1) % n, d.alpha_ns, d.bw});
+        if (d.bidirectional && n > 2) out.push_back({i, (i + n - 1) % n, d.alpha_ns, d.bw});
+      }
+      return TACOS_OK;
+    case TACOS_DIM_FC:
+      for (uint32_t i = 0; i < n; ++i)
+        for (uint32_t j = 0; j < n; ++j)
+          if (i != j) out.push_back({i, j, d.alpha_ns, d.bw});
+      return TACOS_OK;
+    case TACOS_DIM_SWITCH: {
+      const uint32_t deg = d.degree;
+      if (deg < 1 || deg > n - 1) return fail(TACOS_E_INVALID_ARG, "switch degree %u outside [1, %u]", deg, n - 1);
+      if (d.bw % deg != 0) return fail(TACOS_E_INVALID_ARG, "switch bandwidth %u not divisible by degree %u", d.bw, deg);
+      if (deg == 1 && d.bidirectional) {  // the paper's bi-directional ring variation, full bandwidth
+        for (uint32_t i = 0; i < n; ++i) {
+          out.push_back({i, (i + 1) % n, d.alpha_ns, d.bw});
+          if (n > 2) out.push_back({i, (i + n - 1) % n, d.alpha_ns, d.bw});
+        }
+        return TACOS_OK;
+      }
+      for (uint32_t i = 0; i < n; ++i)
+        for (uint32_t s = 1; s <= deg; ++s) out.push_back({i, (i + s) % n, d.alpha_ns, d.bw / deg});
+      return TACOS_OK;
+    }
+    case TACOS_DIM_PATH:
+      for (uint32_t i = 0; i < n; ++i) {
+        if (i + 1 < n) out.push_back({i, i + 1, d.alpha_ns, d.bw});
+        if (i >= 1) out.push_back({i, i - 1, d.alpha_ns, d.bw});
+      }
+      return TACOS_OK;
+    default:
+      return fail(TACOS_E_INVALID_ARG, "unknown dimension kind %d", d.kind);
+  }
+}
+}  // namespace
+
+extern "C" int tacos_build_hierarchical(const tacos_dim_spec *dims, uint32_t n_dims, int32_t *n_npus,
+                                        int32_t *n_links, int32_t *src, int32_t *dst, uint32_t *alpha_ns,
+                                        uint32_t *bw, int64_t capacity) {
+  if (!dims || n_dims == 0 || !n_npus || !n_links) return fail(TACOS_E_INVALID_ARG, "null argument");
+  try {
+    std::vector<std::vector<DimLink>> per(n_dims);
+    std::vector<std::vector<uint32_t>> start(n_dims);  // per dim: links of coordinate c at [start[c], start[c+1])
+    uint64_t N = 1;
+    for (uint32_t i = 0; i < n_dims; ++i) {
+      int rc = dim_links(dims[i], per[i]);
+      if (rc) return rc;
+      N *= dims[i].n;
+      if (N >= (1ull << 31)) return fail(TACOS_E_INVALID_ARG, "too many NPUs");
+      auto &st = start[i];
+      st.assign(dims[i].n + 1, 0u);
+      for (const DimLink &l : per[i]) st[l.a + 1]++;
+      for (uint32_t c = 0; c < dims[i].n; ++c) st[c + 1] += st[c];
+      std::stable_sort(per[i].begin(), per[i].end(), [](const DimLink &x, const DimLink &y) { return x.a < y.a; });
+    }
+    uint64_t L = 0;
+    for (uint32_t i = 0; i < n_dims; ++i) L += per[i].size() * (N / dims[i].n);
+    if (L >= (1ull << 31)) return fail(TACOS_E_INVALID_ARG, "too many links");
+    *n_npus = (int32_t)N;
+    *n_links = (int32_t)L;
+    if (capacity == 0) return TACOS_OK;
+    if ((uint64_t)capacity < L) return fail(TACOS_E_CAPACITY, "capacity %lld < %llu links", (long long)capacity, (unsigned long long)L);
+    if (!src || !dst || !alpha_ns || !bw) return fail(TACOS_E_INVALID_ARG, "null output array");
+    uint64_t k = 0;
+    std::vector<uint32_t> coord(n_dims);
+    for (uint64_t x = 0; x < N; ++x) {
+      uint64_t r = x;
+      for (uint32_t i = 0; i < n_dims; ++i) {
+        coord[i] = (uint32_t)(r % dims[i].n);
+        r /= dims[i].n;
+      }
+      uint64_t stride = 1;
+      for (uint32_t i = 0; i < n_dims; ++i) {
+        const uint32_t c = coord[i];
+        for (uint32_t e = start[i][c]; e < start[i][c + 1]; ++e) {
+          const DimLink &l = per[i][e];
+          src[k] = (int32_t)x;
+          dst[k] = (int32_t)(x + ((int64_t)l.b - (int64_t)c) * (int64_t)stride);
+          alpha_ns[k] = l.alpha;
+          bw[k] = l.bw;
+          ++k;
+        }
+        stride *= dims[i].n;
+      }
+    }
+    return TACOS_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  }
+}
+
+extern "C" int tacos_remove_npus(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst,
+                                 const uint32_t *alpha_ns, const uint32_t *bw, const int32_t *removed,
+                                 uint32_t n_removed, int32_t *out_n_npus, int32_t *out_n_links, int32_t *out_src,
+                                 int32_t *out_dst, uint32_t *out_alpha, uint32_t *out_bw, int64_t capacity,
+                                 int32_t *old_id) {
+  if (n_npus < 1 || n_links < 0 || !out_n_npus || !out_n_links || (n_links && (!src || !dst || !alpha_ns || !bw)) ||
+      (n_removed && !removed))
+    return fail(TACOS_E_INVALID_ARG, "bad argument");
+  try {
+    std::vector<char> gone(n_npus, 0);
+    for (uint32_t i = 0; i < n_removed; ++i) {
+      if (removed[i] < 0 || removed[i] >= n_npus) return fail(TACOS_E_INVALID_ARG, "removed NPU %d out of range", removed[i]);
+      gone[removed[i]] = 1;
+    }
+    std::vector<int32_t> nid(n_npus, -1);
+    int32_t n2 = 0;
+    for (int32_t x = 0; x < n_npus; ++x)
+      if (!gone[x]) {
+        if (old_id && capacity > n2) old_id[n2] = x;
+        nid[x] = n2++;
+      }
+    int64_t L2 = 0;
+    for (int32_t l = 0; l < n_links; ++l)
+      if (src[l] >= 0 && src[l] < n_npus && dst[l] >= 0 && dst[l] < n_npus && !gone[src[l]] && !gone[dst[l]]) ++L2;
+    *out_n_npus = n2;
+    *out_n_links = (int32_t)L2;
+    if (capacity == 0) return TACOS_OK;
+    if (capacity < L2) return fail(TACOS_E_CAPACITY, "capacity %lld < %lld links", (long long)capacity, (long long)L2);
+    if (!out_src || !out_dst || !out_alpha || !out_bw) return fail(TACOS_E_INVALID_ARG, "null output array");
+    int64_t k = 0;
+    for (int32_t l = 0; l < n_links; ++l) {
+      if (src[l] < 0 || src[l] >= n_npus || dst[l] < 0 || dst[l] >= n_npus) continue;
+      if (gone[src[l]] || gone[dst[l]]) continue;
+      out_src[k] = nid[src[l]];
+      out_dst[k] = nid[dst[l]];
+      out_alpha[k] = alpha_ns[l];
+      out_bw[k] = bw[l];
+      ++k;
+    }
+    return TACOS_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  }
+}

@@ -254,3 +254,25 @@ def test_determinism(T):
     a = [T.synthesize(t, "AR", 1, 1 << 20, 32) for _ in range(3)]
     for b in a[1:]:
         assert b.sends.tobytes() == a[0].sends.tobytes() and b.result == a[0].result
+
+
+def test_paper_512_ring_fc_switch_asymmetric(T):
+    """The paper's own 512-NPU scalability system (Ring(2) x FC(4) x Switch(64, d=1),
+    P:L288-289, built with the library front-end): asymmetric, so the RS is
+    searched on G^T (sigma = 1) -- parity on 8 seeds."""
+    dims = [{"kind": "ring", "n": 2, "bw": 200}, {"kind": "fc", "n": 4, "bw": 100},
+            {"kind": "switch", "n": 64, "degree": 1, "bw": 50}]
+    n, src, dst, al, bw = T.tacos_build_hierarchical(dims)
+    topo = W.Topology(n, src, dst, al, bw)
+    syn, sch, _ = run_both(T, topo, 1, 1 << 20, "AR", 8)
+    assert_parity(syn, sch, "AR")
+    assert syn.rs is not syn.ag
+
+
+def test_table_iv_faulty_mesh(T):
+    """Table IV: 4 x 4 mesh without NPUs 7 and 9, All-Reduce."""
+    m = W.mesh2d(4, 4)
+    n2, src, dst, al, bw, _ = T.tacos_remove_npus(16, m.src, m.dst, m.alpha_ns, m.bw, [7, 9])
+    topo = W.Topology(n2, src, dst, al, bw)
+    syn, sch, _ = run_both(T, topo, 1, 1 << 20, "AR", 16)
+    assert_parity(syn, sch, "AR")

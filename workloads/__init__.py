@@ -17,6 +17,7 @@ from .topologies import (  # noqa: F401
     mesh2d,
     torus,
     hypercube,
+    ring_fc_switch,
     switch_hypercube_hybrid,
     random_strongly_connected,
     remove_undirected_links,

@@ -156,6 +156,28 @@ def switch_hypercube_hybrid(groups: int = 16, group_size: int = 16, bw_intra: in
     return _mk(groups * group_size, links, f"switch{group_size}x{groups}_hypercube")
 
 
+def ring_fc_switch(ring: int = 2, fc: int = 4, switch: int = 64, bw_ring: int = 200, bw_fc: int = 100,
+                   bw_switch: int = 50, alpha: int = ALPHA_NS) -> Topology:
+    """The paper's scalability system Ring_FullyConnected_Switch ("3D
+    topology of Ring_FullyConnected_Switch, node size 2x4, 200_100_50 GB/s",
+    P:L289 "degree-max unwinding for scale-up switches and degree-1 for
+    scale-out"): NPU id = r + ring*(f + fc*s); per NPU: ring link(s), FC links,
+    then the scale-out switch unwound with degree 1 (a uni-directional ring)."""
+    n = ring * fc * switch
+    links = []
+    for x in range(n):
+        r, f, s = x % ring, (x // ring) % fc, x // (ring * fc)
+        base_r, base_f = x - r, x - f * ring
+        links.append((x, base_r + (r + 1) % ring, alpha, bw_ring))
+        if ring > 2:
+            links.append((x, base_r + (r - 1) % ring, alpha, bw_ring))
+        for g in range(fc):
+            if g != f:
+                links.append((x, base_f + g * ring, alpha, bw_fc))
+        links.append((x, x + (((s + 1) % switch) - s) * ring * fc, alpha, bw_switch))
+    return _mk(n, links, f"ring{ring}_fc{fc}_switch{switch}")
+
+
 def is_strongly_connected(n: int, src: np.ndarray, dst: np.ndarray) -> bool:
     """Plain BFS from node 0 on G and on G^T."""
     if n <= 1:
@@ -255,6 +277,10 @@ def config(i: int) -> Workload:
         return Workload("c5_switch_hypercube_fail5_ar", topo, 1, 1 * MiB, "AR", 256,
                         note="16 x FC(16) switch groups + 4-D hypercube, 5% undirected links failed, AR, 256 seeds",
                         extra={"failed_undirected": failed.tolist()})
+    if i == 6 or i == "ctx":
+        return Workload("ctx_ring2_fc4_switch64_ar", ring_fc_switch(2, 4, 64, 200, 100, 50), 1, 1 * MiB, "AR", 64,
+                        note="paper's 512-NPU Ring(2) x FC(4) x Switch(64, d=1), 200/100/50 GB/s (P:L288-289, "
+                             "P:L354); asymmetric: the RS is searched on G^T")
     raise ValueError(i)
 
 
