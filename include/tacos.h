@@ -267,6 +267,49 @@ int tacos_eval(const tacos_topology *topo, const tacos_synth_params *p, const ta
                tacos_eval_report *out);
 
 /* ---------------------------------------------------------------------- */
+/* Continuous-time evaluation and baselines (host)       */
+/* ---------------------------------------------------------------------- */
+
+/* Replay `sends` in continuous time ("time domain translator",
+ * P:L299 queueing link congestion): a send on link l lasts
+ * alpha_l + chunk_bytes / bw_l ns (unrounded); each link serves its
+ * sends one at a time, first come first served in the schedule's order of
+ * (t_start, position in the array); a send starts when its link is free and
+ * its input is ready:
+ *   AG-type send (c, a->b): chunk c available at a (initially held, or the end
+ *     of the send that delivered it to a);
+ *   RS-type send (c, a->b) (RS phase of an RS/AR): every RS send of chunk c
+ *     into a has ended (a's partial sum is complete; mirror of the AG rule);
+ *   AR: the first half of the (t_start, link)-sorted sends is the RS phase;
+ *     in the AG phase the owner of c starts from the end of its RS inputs.
+ * The schedule's own order must be a topological order of these
+ * dependencies (true for TACOS and baseline schedules).  Reports the
+ * collective time and the RS phase end, in ns (double). */
+typedef struct {
+  double T_ns;        /* last arrival */
+  double T_rs_ns;     /* AR/RS: end of the RS phase */
+  double max_link_busy_ns; /* busiest link's total occupancy */
+  uint64_t n_sends;
+} tacos_cont_report;
+int tacos_eval_continuous(const tacos_topology *topo, const tacos_synth_params *p, const tacos_send *sends,
+                          uint64_t n_sends, tacos_cont_report *out);
+
+/* Baseline collective algorithms as schedules ("Ring and Direct
+ * collective communication algorithms as two baselines"; P:L120 xy-routing):
+ *   TACOS_BASELINE_RING:   logical ring over NPU ids 0..N-1; in step j NPU i
+ *                          forwards the chunks of NPU (i - j) mod N to NPU i+1;
+ *   TACOS_BASELINE_DIRECT: every NPU sends each of its chunks to every NPU.
+ * Each logical transfer follows a shortest path in hops (BFS visiting out-links
+ * in link-id order; on a mesh in canonical order this is xy routing); every hop
+ * is one send.  t_start is a logical order key (step and hop), t_end =
+ * t_start + w: evaluate them with tacos_eval_continuous (they are not
+ * congestion-free).  RS = time mirror of the AG on G^T, AR = RS then AG.
+ * Call with capacity 0 to get *n_out. */
+enum { TACOS_BASELINE_RING = 0, TACOS_BASELINE_DIRECT = 1 };
+int tacos_baseline(const tacos_topology *topo, const tacos_synth_params *p, int32_t algorithm, tacos_send *out,
+                   uint64_t capacity, uint64_t *n_out);
+
+/* ---------------------------------------------------------------------- */
 /* Topology front-end (host)                             */
 /* ---------------------------------------------------------------------- */
 

@@ -83,6 +83,15 @@ class tacos_winner(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
 
 
+class tacos_cont_report(ctypes.Structure):
+    _fields_ = [("T_ns", ctypes.c_double), ("T_rs_ns", ctypes.c_double), ("max_link_busy_ns", ctypes.c_double),
+                ("n_sends", ctypes.c_uint64)]
+
+
+TACOS_BASELINE_RING, TACOS_BASELINE_DIRECT = 0, 1
+BASELINES = {"ring": TACOS_BASELINE_RING, "direct": TACOS_BASELINE_DIRECT}
+
+
 class tacos_dim_spec(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("n", ctypes.c_uint32), ("degree", ctypes.c_uint32),
                 ("bidirectional", ctypes.c_uint32), ("alpha_ns", ctypes.c_uint32), ("bw", ctypes.c_uint32)]
@@ -137,6 +146,10 @@ SIGNATURES = {
     "tacos_plan_stats": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_result), _VP]),
     "tacos_eval": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_synth_params), _VP, ctypes.c_uint64,
                                   ctypes.POINTER(tacos_eval_report)]),
+    "tacos_eval_continuous": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_synth_params), _VP, ctypes.c_uint64,
+                                             ctypes.POINTER(tacos_cont_report)]),
+    "tacos_baseline": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_synth_params), ctypes.c_int32, _VP, ctypes.c_uint64,
+                                      _U64P]),
     "tacos_build_hierarchical": (ctypes.c_int, [ctypes.POINTER(tacos_dim_spec), ctypes.c_uint32, _I32P, _I32P, _I32P,
                                                 _I32P, _U32P, _U32P, ctypes.c_int64]),
     "tacos_remove_npus": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _I32P, _I32P, _U32P, _U32P, _I32P,
@@ -532,3 +545,28 @@ def tacos_remove_npus(n_npus, src, dst, alpha_ns, bw, removed):
                                  _ptr(oid, ctypes.c_int32)), "tacos_remove_npus")
     k = m2.value
     return n2.value, os_[:k].copy(), od_[:k].copy(), oa_[:k].copy(), ob_[:k].copy(), oid[:n2.value].copy()
+
+
+# --------------------------------------------------------------------------
+# continuous-time evaluation and baselines (f3)
+# --------------------------------------------------------------------------
+def evaluate_continuous(topo: Topology, sends: np.ndarray, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20,
+                        pre=None, post=None, n_chunks=0) -> dict:
+    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1, 0, 0, 1, 0, pre, post, n_chunks)
+    rep = tacos_cont_report()
+    s_ = np.ascontiguousarray(sends, dtype=SEND_DTYPE)
+    _check(load_library().tacos_eval_continuous(topo.handle, ctypes.byref(p), s_.ctypes.data, s_.shape[0],
+                                                ctypes.byref(rep)), "tacos_eval_continuous")
+    return {"T_ns": rep.T_ns, "T_rs_ns": rep.T_rs_ns, "max_link_busy_ns": rep.max_link_busy_ns, "n_sends": rep.n_sends}
+
+
+def baseline(topo: Topology, algorithm="ring", collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20) -> np.ndarray:
+    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1)
+    lib = load_library()
+    n = ctypes.c_uint64()
+    alg = BASELINES[algorithm] if isinstance(algorithm, str) else int(algorithm)
+    _check(lib.tacos_baseline(topo.handle, ctypes.byref(p), alg, None, 0, ctypes.byref(n)), "tacos_baseline")
+    out = np.zeros(max(n.value, 1), dtype=SEND_DTYPE)
+    _check(lib.tacos_baseline(topo.handle, ctypes.byref(p), alg, out.ctypes.data, n.value, ctypes.byref(n)),
+           "tacos_baseline")
+    return out[: n.value]

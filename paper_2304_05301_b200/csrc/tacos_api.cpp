@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -1349,6 +1350,257 @@ extern "C" int tacos_remove_npus(int32_t n_npus, int32_t n_links, const int32_t 
       out_alpha[k] = alpha_ns[l];
       out_bw[k] = bw[l];
       ++k;
+    }
+    return TACOS_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Continuous-time evaluation (f3) and the Ring
+// / Direct baselines.
+// ---------------------------------------------------------------------------
+namespace {
+int params_chunks(const tacos_topology *t, const tacos_synth_params *p, uint32_t &C, std::vector<uint32_t> &pre,
+                  uint32_t &W0) {
+  const uint32_t N = (uint32_t)t->N;
+  if (p->collective == TACOS_CUSTOM) {
+    C = p->n_chunks;
+    W0 = (C + 31) / 32;
+    pre.assign(p->pre_bits, p->pre_bits + (size_t)N * W0);
+  } else {
+    C = N * p->chunks_per_npu;
+    W0 = (C + 31) / 32;
+    pre.assign((size_t)N * W0, 0u);
+    for (uint32_t c = 0; c < C; ++c) {
+      const uint32_t x = c / p->chunks_per_npu;
+      pre[(size_t)x * W0 + (c >> 5)] |= 1u << (c & 31);
+    }
+  }
+  return TACOS_OK;
+}
+}  // namespace
+
+extern "C" int tacos_eval_continuous(const tacos_topology *t, const tacos_synth_params *p, const tacos_send *sends,
+                                     uint64_t n_sends, tacos_cont_report *out) {
+  if (!t || !p || !out || (!sends && n_sends)) return fail(TACOS_E_INVALID_ARG, "null argument");
+  int rc = validate_params(p);
+  if (rc) return rc;
+  try {
+    std::memset(out, 0, sizeof(*out));
+    const uint32_t N = (uint32_t)t->N, L = (uint32_t)t->L;
+    std::vector<double> dur(L);
+    for (uint32_t l = 0; l < L; ++l) dur[l] = (double)t->alpha[l] + (double)p->chunk_bytes / (double)t->bw[l];
+    uint32_t C, W0;
+    std::vector<uint32_t> pre;
+    params_chunks(t, p, C, pre, W0);
+    std::vector<uint64_t> ord(n_sends);
+    for (uint64_t i = 0; i < n_sends; ++i) {
+      const tacos_send &s = sends[i];
+      if (s.link >= L || s.chunk >= C || s.src != (uint32_t)t->src[s.link] || s.dst != (uint32_t)t->dst[s.link])
+        return fail(TACOS_E_VERIFY, "send %llu does not match its link", (unsigned long long)i);
+      ord[i] = i;
+    }
+    std::stable_sort(ord.begin(), ord.end(), [&](uint64_t a, uint64_t b) { return sends[a].t_start < sends[b].t_start; });
+    const bool ar = p->collective == TACOS_ALL_REDUCE, rs = p->collective == TACOS_REDUCE_SCATTER;
+    uint64_t n_rs = ar ? n_sends / 2 : (rs ? n_sends : 0);
+    if (ar) {  // phase split by (t_start, link), as tacos_eval
+      std::vector<uint64_t> o2(ord);
+      std::stable_sort(o2.begin(), o2.end(), [&](uint64_t a, uint64_t b) {
+        return sends[a].t_start != sends[b].t_start ? sends[a].t_start < sends[b].t_start : sends[a].link < sends[b].link;
+      });
+      std::vector<char> in_rs(n_sends, 0);
+      for (uint64_t j = 0; j < n_rs; ++j) in_rs[o2[j]] = 1;
+      std::stable_partition(ord.begin(), ord.end(), [&](uint64_t i) { return in_rs[i] != 0; });
+    }
+    const double kInf = std::numeric_limits<double>::infinity();
+    std::vector<double> link_free(L, 0.0), busy(L, 0.0);
+    std::vector<double> rs_in((size_t)N * C, 0.0);
+    double T_rs = 0.0, T = 0.0;
+    for (uint64_t j = 0; j < n_rs; ++j) {  // reduction phase: a sends once its partial is complete
+      const tacos_send &s = sends[ord[j]];
+      const double ready = rs_in[(size_t)s.src * C + s.chunk];
+      const double st = std::max(ready, link_free[s.link]);
+      const double en = st + dur[s.link];
+      link_free[s.link] = en;
+      busy[s.link] += dur[s.link];
+      double &r = rs_in[(size_t)s.dst * C + s.chunk];
+      r = std::max(r, en);
+      T_rs = std::max(T_rs, en);
+    }
+    std::vector<double> avail((size_t)N * C, kInf);
+    for (uint32_t x = 0; x < N; ++x)
+      for (uint32_t c = 0; c < C; ++c)
+        if ((pre[(size_t)x * W0 + (c >> 5)] >> (c & 31)) & 1u) avail[(size_t)x * C + c] = ar ? std::max(T_rs, rs_in[(size_t)x * C + c]) : 0.0;
+    T = T_rs;
+    for (uint64_t j = n_rs; j < n_sends; ++j) {  // data movement phase
+      const tacos_send &s = sends[ord[j]];
+      const double ready = avail[(size_t)s.src * C + s.chunk];
+      if (ready == kInf)
+        return fail(TACOS_E_VERIFY, "send %llu (chunk %u at NPU %u) departs before its chunk is available",
+                    (unsigned long long)ord[j], s.chunk, s.src);
+      const double st = std::max(ready, link_free[s.link]);
+      const double en = st + dur[s.link];
+      link_free[s.link] = en;
+      busy[s.link] += dur[s.link];
+      double &a = avail[(size_t)s.dst * C + s.chunk];
+      a = std::min(a, en);
+      T = std::max(T, en);
+    }
+    out->T_ns = T;
+    out->T_rs_ns = T_rs;
+    out->n_sends = n_sends;
+    for (uint32_t l = 0; l < L; ++l) out->max_link_busy_ns = std::max(out->max_link_busy_ns, busy[l]);
+    return TACOS_OK;
+  } catch (const std::bad_alloc &) {
+    return fail(TACOS_E_NOMEM, "host allocation failed");
+  }
+}
+
+namespace {
+// Shortest paths in hops from s: BFS visiting out-links in link-id order
+// (orientation o: 0 = G, 1 = G^T).  parent[x] = link into x on the path.
+void bfs_parents(const tacos_topology *t, int o, uint32_t s, std::vector<int32_t> &parent) {
+  const uint32_t N = (uint32_t)t->N;
+  parent.assign(N, -1);
+  std::vector<char> seen(N, 0);
+  std::vector<uint32_t> q{s};
+  seen[s] = 1;
+  // out-links of x in G are the in-links of x in G^T's CSR (orientation 1 groups by src)
+  const int oo = 1 - o;
+  for (size_t h = 0; h < q.size(); ++h) {
+    const uint32_t x = q[h];
+    for (uint32_t e = t->in_ptr[oo][x]; e < t->in_ptr[oo][x + 1]; ++e) {
+      const uint32_t y = t->pos_src[oo][e];  // other endpoint
+      if (!seen[y]) {
+        seen[y] = 1;
+        parent[y] = (int32_t)t->pos_lid[oo][e];
+        q.push_back(y);
+      }
+    }
+  }
+}
+
+struct LSend {
+  uint32_t chunk, a, b, link;
+  uint64_t key;
+};
+
+// AG baseline on orientation o (links as given for o = 0, reversed for o = 1).
+int baseline_ag(const tacos_topology *t, uint32_t k, int alg, int o, std::vector<LSend> &out) {
+  const uint32_t N = (uint32_t)t->N;
+  out.clear();
+  std::vector<std::vector<int32_t>> par(N);
+  for (uint32_t s = 0; s < N; ++s) bfs_parents(t, o, s, par[s]);
+  auto path = [&](uint32_t s, uint32_t d, std::vector<uint32_t> &links) -> bool {
+    links.clear();
+    uint32_t x = d;
+    while (x != s) {
+      const int32_t l = par[s][x];
+      if (l < 0) return false;
+      links.push_back((uint32_t)l);
+      x = (uint32_t)(o == 0 ? t->src[l] : t->dst[l]);
+    }
+    std::reverse(links.begin(), links.end());
+    return true;
+  };
+  auto ends = [&](uint32_t l, uint32_t &a, uint32_t &b) {
+    a = (uint32_t)(o == 0 ? t->src[l] : t->dst[l]);
+    b = (uint32_t)(o == 0 ? t->dst[l] : t->src[l]);
+  };
+  std::vector<uint32_t> hops;
+  if (alg == TACOS_BASELINE_RING) {
+    // logical ring i -> i+1 on G; on G^T (the RS, mirrored back onto G) i -> i-1, so
+    // the mirrored reduction ring runs i-1 -> i along G's own direction
+    auto succ = [&](uint32_t i) { return o == 0 ? (i + 1) % N : (i + N - 1) % N; };
+    auto pred_owner = [&](uint32_t i, uint32_t j) { return o == 0 ? (i + N - j) % N : (i + j) % N; };
+    uint64_t H = 1;
+    for (uint32_t i = 0; i < N; ++i) {
+      if (!path(i, succ(i), hops)) return fail(TACOS_E_UNREACHABLE, "no path %u -> %u", i, succ(i));
+      H = std::max<uint64_t>(H, hops.size());
+    }
+    for (uint32_t j = 0; j + 1 < N; ++j)
+      for (uint32_t i = 0; i < N; ++i) {
+        const uint32_t owner = pred_owner(i, j);
+        path(i, succ(i), hops);
+        for (uint32_t h = 0; h < hops.size(); ++h)
+          for (uint32_t q = 0; q < k; ++q) {
+            LSend s;
+            s.chunk = owner * k + q;
+            ends(hops[h], s.a, s.b);
+            s.link = hops[h];
+            s.key = (uint64_t)j * H + h;
+            out.push_back(s);
+          }
+      }
+  } else {
+    for (uint32_t owner = 0; owner < N; ++owner)
+      for (uint32_t d = 0; d < N; ++d) {
+        if (d == owner) continue;
+        if (!path(owner, d, hops)) return fail(TACOS_E_UNREACHABLE, "no path %u -> %u", owner, d);
+        for (uint32_t h = 0; h < hops.size(); ++h)
+          for (uint32_t q = 0; q < k; ++q) {
+            LSend s;
+            s.chunk = owner * k + q;
+            ends(hops[h], s.a, s.b);
+            s.link = hops[h];
+            s.key = h;
+            out.push_back(s);
+          }
+      }
+  }
+  std::stable_sort(out.begin(), out.end(), [](const LSend &x, const LSend &y) { return x.key < y.key; });
+  return TACOS_OK;
+}
+}  // namespace
+
+extern "C" int tacos_baseline(const tacos_topology *t, const tacos_synth_params *p, int32_t algorithm, tacos_send *out,
+                              uint64_t capacity, uint64_t *n_out) {
+  if (!t || !p || !n_out) return fail(TACOS_E_INVALID_ARG, "null argument");
+  int rc = validate_params(p);
+  if (rc) return rc;
+  if (p->collective == TACOS_CUSTOM) return fail(TACOS_E_INVALID_ARG, "baselines are defined for AG / RS / AR");
+  if (algorithm != TACOS_BASELINE_RING && algorithm != TACOS_BASELINE_DIRECT)
+    return fail(TACOS_E_INVALID_ARG, "unknown baseline %d", algorithm);
+  try {
+    std::vector<uint32_t> w;
+    if ((rc = link_costs(t, p->chunk_bytes, p->time_unit_ns ? p->time_unit_ns : 1u, w))) return rc;
+    std::vector<LSend> ag, rsv;
+    const int coll = p->collective;
+    if (coll != TACOS_REDUCE_SCATTER)
+      if ((rc = baseline_ag(t, p->chunks_per_npu, algorithm, 0, ag))) return rc;
+    if (coll != TACOS_ALL_GATHER)
+      if ((rc = baseline_ag(t, p->chunks_per_npu, algorithm, 1, rsv))) return rc;
+    const uint64_t n = ag.size() + rsv.size();
+    *n_out = n;
+    if (capacity == 0) return TACOS_OK;
+    if (capacity < n) return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)capacity, (unsigned long long)n);
+    if (!out) return fail(TACOS_E_INVALID_ARG, "null output");
+    uint64_t kmax = 0;
+    for (const LSend &s : rsv) kmax = std::max(kmax, s.key);
+    uint64_t i = 0;
+    // RS: time mirror of the AG on G^T, landing on G's links (R9)
+    for (auto it = rsv.rbegin(); it != rsv.rend(); ++it) {
+      tacos_send s;
+      s.chunk = it->chunk;
+      s.src = it->b;
+      s.dst = it->a;
+      s.link = it->link;
+      s.t_start = kmax - it->key;
+      s.t_end = s.t_start + w[s.link];
+      out[i++] = s;
+    }
+    const uint64_t shift = rsv.empty() ? 0 : kmax + 1;
+    for (const LSend &x : ag) {
+      tacos_send s;
+      s.chunk = x.chunk;
+      s.src = x.a;
+      s.dst = x.b;
+      s.link = x.link;
+      s.t_start = x.key + shift;
+      s.t_end = s.t_start + w[s.link];
+      out[i++] = s;
     }
     return TACOS_OK;
   } catch (const std::bad_alloc &) {
