@@ -74,7 +74,12 @@ typedef enum {
 
 enum {
   TACOS_FLAG_NO_SCHEDULE = 1u,   /* search only: no send records, time and seed only */
-  TACOS_FLAG_KEEP_SEED_TIMES = 2u /* keep the per-seed collective times */
+  TACOS_FLAG_KEEP_SEED_TIMES = 2u, /* keep the per-seed collective times */
+  /* Paper-literal variant (reading R21): chunk-first
+   * matching with replacement of outdated transmissions
+   * instead of the link-first walk with persistent claims (R1, R4).  One CTA per
+   * seed, in-degree <= 32; cancelled transmissions leave the schedule. */
+  TACOS_FLAG_LITERAL = 4u
 };
 
 typedef struct tacos_topology tacos_topology; /* opaque */
@@ -119,6 +124,7 @@ typedef struct {
   uint32_t winner_local; /* bit 0: the AG phase was emitted here; bit 1: the RS phase was emitted here
                             (the winning seed of that phase belongs to this shard) */
   uint64_t best_key_ag, best_key_rs; /* (T << 20) | global seed index, see tacos_plan_best_keys */
+  uint64_t cancelled;  /* TACOS_FLAG_LITERAL: transmissions dropped as duplicates or replaced */
 } tacos_result;
 
 typedef enum {

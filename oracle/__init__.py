@@ -71,6 +71,8 @@ def lib():
                 ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64, u64p, u64p, u64p,
             ]
             l.oracle_greedy.restype = ctypes.c_int
+            l.oracle_greedy_literal.argtypes = l.oracle_greedy.argtypes
+            l.oracle_greedy_literal.restype = ctypes.c_int
             _lib = l
     return _lib
 
@@ -125,12 +127,14 @@ class GreedyResult:
     E: int
     seed: int
     sigma: int
+    X: int = 0  # cancelled sends (paper-literal variant: duplicates + replaced outdated transmissions)
 
 
 def greedy(n_npus: int, src: np.ndarray, dst: np.ndarray, w: np.ndarray, n_chunks: int, k: int, seed: int,
            sigma: int = 0, pre: Optional[np.ndarray] = None, post: Optional[np.ndarray] = None,
-           record: bool = True) -> GreedyResult:
-    """One TACOS-Greedy synthesis (SURVEY §8(c) pseudo-code)."""
+           record: bool = True, literal: bool = False) -> GreedyResult:
+    """One TACOS-Greedy synthesis (SURVEY §8(c) pseudo-code); literal=True runs the
+    paper-literal chunk-first variant with chunk replacement (row f1, reading R21)."""
     src = np.ascontiguousarray(src, dtype=np.int32)
     dst = np.ascontiguousarray(dst, dtype=np.int32)
     w = np.ascontiguousarray(w, dtype=np.uint64)
@@ -146,8 +150,9 @@ def greedy(n_npus: int, src: np.ndarray, dst: np.ndarray, w: np.ndarray, n_chunk
     sends = np.zeros(max(cap, 1), dtype=SEND_DTYPE)
     n_sends = ctypes.c_uint64(0)
     T = ctypes.c_uint64(0)
-    stats = np.zeros(4, dtype=np.uint64)
-    rc = lib().oracle_greedy(
+    stats = np.zeros(5, dtype=np.uint64)
+    fn = lib().oracle_greedy_literal if literal else lib().oracle_greedy
+    rc = fn(
         n_npus, src.shape[0], _p(src, ctypes.c_int32), _p(dst, ctypes.c_int32), _p(w, ctypes.c_uint64),
         n_chunks, k, pre_p, post_p, ctypes.c_uint64(seed & (2**64 - 1)), sigma,
         sends.ctypes.data if record else None, cap, ctypes.byref(n_sends), ctypes.byref(T), _p(stats, ctypes.c_uint64),
@@ -155,7 +160,7 @@ def greedy(n_npus: int, src: np.ndarray, dst: np.ndarray, w: np.ndarray, n_chunk
     if rc != OK:
         raise OracleError(rc, f"greedy seed={seed} sigma={sigma}")
     return GreedyResult(int(T.value), sends[: int(n_sends.value)] if record else sends[:0], int(stats[0]),
-                        int(stats[1]), int(stats[2]), int(stats[3]), seed, sigma)
+                        int(stats[1]), int(stats[2]), int(stats[3]), seed, sigma, int(stats[4]))
 
 
 # --------------------------------------------------------------------------
@@ -212,7 +217,8 @@ class Synthesis:
 
 def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "AR", seeds: Sequence[int] = (0,),
                time_unit_ns: int = 1, pre: Optional[np.ndarray] = None, post: Optional[np.ndarray] = None,
-               threads: Optional[int] = None, record: bool = True, n_chunks: Optional[int] = None) -> Synthesis:
+               threads: Optional[int] = None, record: bool = True, n_chunks: Optional[int] = None,
+               literal: bool = False) -> Synthesis:
     """Best-of-S TACOS-Greedy synthesis of AG / RS / AR (or CUSTOM with pre/post,
     collective 'CUSTOM').  seeds are the 64-bit Philox keys; ties go to the
     lowest position in ``seeds`` (R11)."""
@@ -229,7 +235,7 @@ def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "A
 
     def run(args):
         s, sig, a, b = args
-        return greedy(n, a, b, w, C, chunks_per_npu, s, sig, pre, post, record)
+        return greedy(n, a, b, w, C, chunks_per_npu, s, sig, pre, post, record, literal)
 
     jobs_ag = [(s, 0, src, dst) for s in seeds]
     rev = reverse_links(src, dst, w)

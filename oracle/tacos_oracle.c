@@ -275,3 +275,223 @@ done:
   free(busy_until); free(cur); free(F); free(in_start); free(in_list);
   return rc;
 }
+
+/*
+ * Paper-literal variant (reading R21).
+ *   chunk-first matching ("first we choose a requested chunk and
+ *   backtrack the NPU ... among candidate links, we can randomly select one"),
+ *   shorter-link-first among the candidates, the arrival-time rule
+ *    and chunk replacement of outdated transmissions:
+ * At each event t:
+ *  (1) arrivals in ascending link id; a copy of a chunk its destination already
+ *      holds (a duplicate) is dropped: its send leaves the schedule;
+ *  (2) done test;
+ *  (3) replacement: an in-flight send whose chunk its destination already holds
+ *      is outdated: cancelled (leaves the schedule), its link is free at t;
+ *  (4) per destination d: R = post[d] - held[d] (chunks in flight to d are
+ *      requested again); Philox block (t_lo, t_hi, d, 0x80000000 | sigma<<16 | 0),
+ *      word 0 -> r0 = floor(u * |R| / 2^32); chunks are visited in ascending id
+ *      from the r0-th smallest member of R, cyclically; for chunk c the
+ *      candidates are d's free in-links not matched at t whose source holds c;
+ *      the candidates of minimal w are kept, and the m-th match (m = 1, 2, ...)
+ *      takes the floor(u * n / 2^32)-th of them (ascending link id) with u = word 0
+ *      of block (t_lo, t_hi, d, 0x80000000 | sigma<<16 | m); stop when d has no
+ *      free unmatched in-link;
+ *  (5) advance to the next busy_until.
+ * stats: [0]=V free in-links at (4), [1]=D, [2]=M sends issued, [3]=E, [4]=X cancelled.
+ * Output: the delivered sends (production order of their issue).
+ */
+int oracle_greedy_literal(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst, const uint64_t *w,
+                          uint32_t n_chunks, uint32_t k, const uint32_t *pre_bits, const uint32_t *post_bits,
+                          uint64_t seed, uint32_t sigma, oracle_send *sends, uint64_t cap, uint64_t *n_sends_out,
+                          uint64_t *T_out, uint64_t *stats) {
+  if (n_npus < 1 || n_links < 0 || n_chunks < 1) return ORACLE_E_INVALID_ARG;
+  const uint32_t N = (uint32_t)n_npus, L = (uint32_t)n_links, C = n_chunks;
+  const uint32_t W = (C + 31) / 32;
+  int rc = ORACLE_OK;
+  uint32_t *held = calloc((size_t)N * W, 4);
+  uint32_t *post = calloc((size_t)N * W, 4);
+  uint64_t *busy_until = calloc(L ? L : 1, 8);
+  uint32_t *cur = malloc((size_t)(L ? L : 1) * 4);
+  uint64_t *issue = malloc((size_t)(L ? L : 1) * 8);   /* index of the link's in-flight send */
+  char *used = calloc(L ? L : 1, 1);
+  uint32_t *in_start = calloc((size_t)N + 1, 4);
+  uint32_t *in_list = malloc((size_t)(L ? L : 1) * 4);
+  uint32_t *cands = malloc((size_t)(L ? L : 1) * 4);
+  /* every issued send, with a cancelled flag; capacity grows */
+  uint64_t n_issued = 0, cap_issued = 1024;
+  oracle_send *issued = malloc(cap_issued * sizeof(oracle_send));
+  char *cancelled = calloc(cap_issued, 1);
+  if (!held || !post || !busy_until || !cur || !issue || !used || !in_start || !in_list || !cands || !issued ||
+      !cancelled) {
+    rc = ORACLE_E_NOMEM;
+    goto done;
+  }
+  uint64_t required = 0;
+  if (pre_bits == NULL) {
+    if ((uint64_t)N * k != C) { rc = ORACLE_E_INVALID_ARG; goto done; }
+    for (uint32_t x = 0; x < N; ++x) {
+      for (uint32_t j = 0; j < k; ++j) bit_set(&held[(size_t)x * W], x * k + j);
+      for (uint32_t c = 0; c < C; ++c) bit_set(&post[(size_t)x * W], c);
+    }
+    required = (uint64_t)C * (N - 1);
+  } else {
+    memcpy(held, pre_bits, (size_t)N * W * 4);
+    memcpy(post, post_bits, (size_t)N * W * 4);
+    for (uint32_t x = 0; x < N; ++x)
+      for (uint32_t c = 0; c < C; ++c) {
+        int a = bit_get(&held[(size_t)x * W], c), b = bit_get(&post[(size_t)x * W], c);
+        if (a && !b) { rc = ORACLE_E_INVALID_ARG; goto done; }
+        if (b && !a) required++;
+      }
+  }
+  for (uint32_t l = 0; l < L; ++l) {
+    if (src[l] < 0 || src[l] >= n_npus || dst[l] < 0 || dst[l] >= n_npus || w[l] < 1) { rc = ORACLE_E_INVALID_ARG; goto done; }
+    cur[l] = NONE;
+    busy_until[l] = 0;
+  }
+  for (uint32_t l = 0; l < L; ++l) in_start[dst[l] + 1]++;
+  for (uint32_t d = 0; d < N; ++d) in_start[d + 1] += in_start[d];
+  {
+    uint32_t *fill = calloc((size_t)N, 4);
+    if (!fill) { rc = ORACLE_E_NOMEM; goto done; }
+    for (uint32_t l = 0; l < L; ++l) in_list[in_start[dst[l]] + fill[dst[l]]++] = l;
+    free(fill);
+  }
+  uint64_t t = 0, delivered = 0, V = 0, D = 0, M = 0, E = 0, X = 0;
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (;;) {
+    /* (1) arrivals, ascending link id; duplicates dropped */
+    for (uint32_t l = 0; l < L; ++l) {
+      if (cur[l] != NONE && busy_until[l] == t) {
+        uint32_t *hd = &held[(size_t)dst[l] * W];
+        if (bit_get(hd, cur[l])) {
+          cancelled[issue[l]] = 1;
+          X += 1;
+        } else {
+          bit_set(hd, cur[l]);
+          delivered += 1;
+        }
+        cur[l] = NONE;
+      }
+    }
+    /* (2) done: copies still in flight are outdated and leave the schedule */
+    if (delivered == required) {
+      *T_out = t;
+      for (uint32_t l = 0; l < L; ++l)
+        if (cur[l] != NONE) {
+          cancelled[issue[l]] = 1;
+          X += 1;
+          cur[l] = NONE;
+        }
+      break;
+    }
+    /* (3) replacement of outdated in-flight sends */
+    for (uint32_t l = 0; l < L; ++l) {
+      if (cur[l] != NONE && bit_get(&held[(size_t)dst[l] * W], cur[l])) {
+        cancelled[issue[l]] = 1;
+        X += 1;
+        cur[l] = NONE;
+        busy_until[l] = t;
+      }
+    }
+    /* (4) chunk-first matching */
+    E += 1;
+    for (uint32_t d = 0; d < N; ++d) {
+      uint32_t n_free = 0;
+      for (uint32_t e = in_start[d]; e < in_start[d + 1]; ++e) {
+        uint32_t l = in_list[e];
+        used[l] = 0;
+        if (cur[l] == NONE) n_free++;
+      }
+      if (n_free == 0) continue;
+      D += 1;
+      V += n_free;
+      const uint32_t *hd = &held[(size_t)d * W], *pd = &post[(size_t)d * W];
+      uint64_t nR = 0;
+      for (uint32_t c = 0; c < C; ++c)
+        if (bit_get(pd, c) && !bit_get(hd, c)) nR++;
+      if (nR == 0) continue;
+      uint32_t ctr[4] = {(uint32_t)t, (uint32_t)(t >> 32), d, 0x80000000u | (sigma << 16)};
+      uint32_t out[4];
+      oracle_philox4x32_10(ctr, key, out);
+      uint64_t r0 = ((uint64_t)out[0] * nR) >> 32;
+      /* start chunk: the r0-th smallest member of R */
+      uint32_t start = 0;
+      {
+        uint64_t seen = 0;
+        for (uint32_t c = 0; c < C; ++c)
+          if (bit_get(pd, c) && !bit_get(hd, c)) {
+            if (seen == r0) { start = c; break; }
+            seen++;
+          }
+      }
+      uint32_t m = 0, n_unmatched = n_free;
+      for (uint32_t i = 0; i < C && n_unmatched > 0; ++i) {
+        const uint32_t c = (start + i) % C;
+        if (!(bit_get(pd, c) && !bit_get(hd, c))) continue;
+        /* candidates: free, unmatched in-links whose source holds c; keep minimal w */
+        uint32_t nc = 0;
+        uint64_t wmin = UINT64_MAX;
+        for (uint32_t e = in_start[d]; e < in_start[d + 1]; ++e) {
+          uint32_t l = in_list[e];
+          if (cur[l] != NONE || used[l]) continue;
+          if (!bit_get(&held[(size_t)src[l] * W], c)) continue;
+          if (w[l] < wmin) { wmin = w[l]; nc = 0; }
+          if (w[l] == wmin) cands[nc++] = l;
+        }
+        if (nc == 0) continue;
+        m += 1;
+        uint32_t ctr2[4] = {(uint32_t)t, (uint32_t)(t >> 32), d, 0x80000000u | (sigma << 16) | m};
+        oracle_philox4x32_10(ctr2, key, out);
+        const uint32_t l = cands[((uint64_t)out[0] * nc) >> 32];
+        if (t > UINT64_MAX / 2 - w[l]) { rc = ORACLE_E_OVERFLOW; goto done; }
+        used[l] = 1;
+        n_unmatched--;
+        cur[l] = c;
+        busy_until[l] = t + w[l];
+        if (n_issued == cap_issued) {
+          cap_issued *= 2;
+          oracle_send *ni = realloc(issued, cap_issued * sizeof(oracle_send));
+          char *nc2 = realloc(cancelled, cap_issued);
+          if (!ni || !nc2) { rc = ORACLE_E_NOMEM; if (ni) issued = ni; if (nc2) cancelled = nc2; goto done; }
+          issued = ni;
+          cancelled = nc2;
+          memset(cancelled + n_issued, 0, cap_issued - n_issued);
+        }
+        issued[n_issued].chunk = c;
+        issued[n_issued].src = (uint32_t)src[l];
+        issued[n_issued].dst = d;
+        issued[n_issued].link = l;
+        issued[n_issued].t_start = t;
+        issued[n_issued].t_end = t + w[l];
+        issue[l] = n_issued;
+        n_issued++;
+        M += 1;
+      }
+    }
+    /* (5) advance */
+    uint64_t t_next = UINT64_MAX;
+    for (uint32_t l = 0; l < L; ++l)
+      if (cur[l] != NONE && busy_until[l] < t_next) t_next = busy_until[l];
+    if (t_next == UINT64_MAX) { rc = ORACLE_E_UNREACHABLE; *T_out = t; break; }
+    t = t_next;
+  }
+  {
+    uint64_t n_out = 0;
+    for (uint64_t i = 0; i < n_issued; ++i) {
+      if (cancelled[i]) continue;
+      if (sends) {
+        if (n_out >= cap) { rc = ORACLE_E_CAPACITY; goto done; }
+        sends[n_out] = issued[i];
+      }
+      n_out++;
+    }
+    *n_sends_out = n_out;
+  }
+  if (stats) { stats[0] = V; stats[1] = D; stats[2] = M; stats[3] = E; stats[4] = X; }
+done:
+  free(held); free(post); free(busy_until); free(cur); free(issue); free(used);
+  free(in_start); free(in_list); free(cands); free(issued); free(cancelled);
+  return rc;
+}

@@ -39,6 +39,7 @@ COLLECTIVES = {"AG": TACOS_ALL_GATHER, "RS": TACOS_REDUCE_SCATTER, "AR": TACOS_A
 
 TACOS_FLAG_NO_SCHEDULE = 1
 TACOS_FLAG_KEEP_SEED_TIMES = 2
+TACOS_FLAG_LITERAL = 4
 
 VIOLATIONS = ("no_such_link", "wrong_duration", "link_overlap", "unheld_at_depart", "duplicate_delivery",
               "post_unmet", "phase_order")
@@ -68,7 +69,7 @@ class tacos_result(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("rs_seed", ctypes.c_uint64), ("n_sends", ctypes.c_uint64),
                 ("matches", ctypes.c_uint64), ("visits", ctypes.c_uint64), ("dest_events", ctypes.c_uint64),
                 ("events", ctypes.c_uint64), ("status", ctypes.c_int32), ("winner_local", ctypes.c_uint32),
-                ("best_key_ag", ctypes.c_uint64), ("best_key_rs", ctypes.c_uint64)]
+                ("best_key_ag", ctypes.c_uint64), ("best_key_rs", ctypes.c_uint64), ("cancelled", ctypes.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -374,8 +375,9 @@ class Schedule:
 
 def synthesize(topo: Topology, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=1, base_seed=0,
                time_unit_ns=1, keep_seed_times=False, no_schedule=False, pre=None, post=None,
-               n_chunks=0) -> Schedule:
-    flags = (TACOS_FLAG_KEEP_SEED_TIMES if keep_seed_times else 0) | (TACOS_FLAG_NO_SCHEDULE if no_schedule else 0)
+               n_chunks=0, literal=False) -> Schedule:
+    flags = ((TACOS_FLAG_KEEP_SEED_TIMES if keep_seed_times else 0) | (TACOS_FLAG_NO_SCHEDULE if no_schedule else 0)
+             | (TACOS_FLAG_LITERAL if literal else 0))
     p, keep = make_params(collective, chunks_per_npu, chunk_bytes, n_seeds, base_seed, 0, time_unit_ns, flags, pre,
                           post, n_chunks)
     h = tacos_synthesize(topo.handle, p)

@@ -452,6 +452,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     const uint32_t W0 = (pt.C + 31u) / 32u;
     const uint32_t vec = (W0 + 3u) / 4u;
     pt.P = std::min<uint32_t>(32u, pow2_at_least((vec + 3u) / 4u));  // up to 4 vectors per lane
+    if (p->flags & TACOS_FLAG_LITERAL) pt.P = 32u;  // literal variant: one warp per destination
     if (const char *env = getenv("TACOS_LANES")) {  // tuning override: lanes per destination row
       const uint32_t want = (uint32_t)atoi(env);
       if (want >= 1 && want <= 32 && (want & (want - 1)) == 0 && want <= pow2_at_least(vec) &&
@@ -521,6 +522,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         for (int32_t d = 0; d < tt->N; ++d) max_deg = std::max(max_deg, tt->in_ptr[o][d + 1] - tt->in_ptr[o][d]);
     }
     g.lay.reg_path = max_deg <= 8u ? 1u : 0u;
+    if (p->flags & TACOS_FLAG_LITERAL) {
+      if (max_deg > 32u) return fail(TACOS_E_INVALID_ARG, "literal variant supports in-degree <= 32 (got %u)", max_deg);
+      if (!g.lay.links_in_smem) return fail(TACOS_E_OVERFLOW, "literal variant: link state does not fit shared memory");
+      g.lay.cluster = 1;
+    }
     if (const char *env = getenv("TACOS_REG_PATH")) g.lay.reg_path = (uint32_t)atoi(env);
     g.job_begin = begin;
     g.job_end = n_jobs;
@@ -595,7 +601,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.required * pt.n_jobs, &vp))) return rc;
       pt.d_rec = reinterpret_cast<Rec *>(vp);
     }
-    if ((rc = dev_alloc(bufs, dev, 8 * 7, &vp))) return rc;
+    if ((rc = dev_alloc(bufs, dev, 8 * 8, &vp))) return rc;
     pt.d_keys = reinterpret_cast<uint64_t *>(vp);
     pt.d_stats = pt.d_keys + 2;
     if ((rc = dev_alloc(bufs, dev, 8 * (size_t)S, &vp))) return rc;
@@ -604,7 +610,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       if ((rc = dev_alloc(bufs, dev, 8 * (size_t)S, &vp))) return rc;
       pt.d_times_rs = reinterpret_cast<uint64_t *>(vp);
     }
-    if (need_rs && record) max_M = std::max(max_M, pt.required);
+    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL)) && record) max_M = std::max(max_M, pt.required);
   }
   if (max_M) {
     pl->sort_bytes = rs_sort_scratch_bytes(max_M);
@@ -659,9 +665,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
 int plan_search(tacos_plan *pl, cudaStream_t st) {
   int rc;
   pl->last_launches = 0;
+  const bool literal = (pl->p.flags & TACOS_FLAG_LITERAL) != 0;
   for (auto &g : pl->groups) {
-    if ((rc = launch_greedy(g.lay, g.P, g.VPL, pl->d_jobs + g.job_begin, g.job_end - g.job_begin, pl->d_outs, st)))
-      return fail(rc, "%s", cuda_error_string());
+    rc = literal ? launch_literal(g.lay, g.VPL, pl->d_jobs + g.job_begin, g.job_end - g.job_begin, pl->d_outs, st)
+                 : launch_greedy(g.lay, g.P, g.VPL, pl->d_jobs + g.job_begin, g.job_end - g.job_begin, pl->d_outs, st);
+    if (rc) return fail(rc, "%s", cuda_error_string());
     pl->last_launches++;
   }
   const uint32_t S = pl->p.n_seeds;
@@ -677,7 +685,7 @@ int plan_search(tacos_plan *pl, cudaStream_t st) {
 // Read keys + stats of every part (one D2H, one sync).
 int plan_read_small(tacos_plan *pl, cudaStream_t st) {
   for (size_t i = 0; i < pl->parts.size(); ++i)
-    CUDA_TRY(cudaMemcpyAsync(pl->h_small + 8 * i, pl->parts[i].d_keys, 7 * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(pl->h_small + 8 * i, pl->parts[i].d_keys, 8 * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return TACOS_OK;
 }
@@ -699,6 +707,7 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   res->dest_events = stats[1];
   res->matches = stats[2];
   res->events = stats[3];
+  res->cancelled = stats[5];
   res->best_key_ag = key_ag;
   res->best_key_rs = key_rs;
   const int32_t st_status = (int32_t)(int64_t)stats[4];
@@ -744,9 +753,17 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   if (need_ag && ag_local) {
     const Rec *rec = pt.d_rec + (size_t)(g_ag - off) * M;
     const uint64_t base = coll == TACOS_ALL_REDUCE ? M : 0;
-    if ((rc = launch_emit_ag(rec, M, t->d_src, t->d_dst, pt.d_w, T_rs, d_sends + base, st)))
-      return fail(rc, "%s", cuda_error_string());
-    pl->last_launches += 1;
+    if (pl->p.flags & TACOS_FLAG_LITERAL) {  // records in delivery order: sort by (t_start, link)
+      uint32_t nl = 0;
+      if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, nullptr, T_ag, pt.L, d_sends + base, pl->d_sort,
+                                    pl->sort_bytes, &nl, st, /*mirror=*/0u, /*shift=*/T_rs)))
+        return fail(rc, "%s", cuda_error_string());
+      pl->last_launches += nl;
+    } else {
+      if ((rc = launch_emit_ag(rec, M, t->d_src, t->d_dst, pt.d_w, T_rs, d_sends + base, st)))
+        return fail(rc, "%s", cuda_error_string());
+      pl->last_launches += 1;
+    }
     emitted += M;
   }
   res->n_sends = emitted;

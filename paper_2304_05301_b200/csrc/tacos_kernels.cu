@@ -127,16 +127,16 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
                                  uint32_t rs_base, uint32_t has_rs, unsigned long long *keys,
                                  unsigned long long *stats, unsigned long long *times_ag,
                                  unsigned long long *times_rs) {
-  __shared__ unsigned long long s_k0, s_k1, s_V, s_D, s_M, s_E;
+  __shared__ unsigned long long s_k0, s_k1, s_V, s_D, s_M, s_E, s_X;
   __shared__ int s_status;
   if (threadIdx.x == 0) {
     s_k0 = s_k1 = kNoKey;
-    s_V = s_D = s_M = s_E = 0ull;
+    s_V = s_D = s_M = s_E = s_X = 0ull;
     s_status = 0;
   }
   __syncthreads();
   const uint32_t n_jobs = has_rs ? rs_base + n_seeds : n_seeds;
-  unsigned long long k0 = kNoKey, k1 = kNoKey, V = 0, D = 0, M = 0, E = 0;
+  unsigned long long k0 = kNoKey, k1 = kNoKey, V = 0, D = 0, M = 0, E = 0, X = 0;
   int st = 0;
   for (uint32_t j = threadIdx.x; j < n_jobs; j += blockDim.x) {
     const JobOut o = outs[j];
@@ -144,6 +144,7 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
     D += o.D;
     M += o.M;
     E += o.E;
+    X += o.pad;
     if (o.status != 0) st = o.status;
     const bool is_rs = has_rs && j >= rs_base;
     const uint32_t i = is_rs ? j - rs_base : j;
@@ -163,6 +164,7 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
   atomicAdd(&s_D, D);
   atomicAdd(&s_M, M);
   atomicAdd(&s_E, E);
+  atomicAdd(&s_X, X);
   if (st != 0) atomicMin(&s_status, st);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -173,6 +175,7 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
     stats[2] = s_M;
     stats[3] = s_E;
     stats[4] = (unsigned long long)(long long)s_status;
+    stats[5] = s_X;
   }
 }
 
@@ -227,12 +230,12 @@ int launch_emit_ag(const Rec *rec, uint64_t M, const uint32_t *src, const uint32
 // RS = mirror of an AG: (c, a->b on l, t0, t1) -> (c, b->a on l', T-t1, T-t0)
 // with l' = rev[l] when G is symmetric (AG searched on G), else l' = l (AG searched on G^T).
 __global__ void rs_keys_kernel(const Rec *__restrict__ rec, uint64_t M, const uint32_t *__restrict__ w,
-                               const int32_t *__restrict__ rev, uint64_t T_rs, uint32_t lbits,
+                               const int32_t *__restrict__ rev, uint64_t T_rs, uint32_t lbits, uint32_t mirror,
                                unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < M; i += (uint64_t)gridDim.x * blockDim.x) {
     const Rec r = rec[i];
-    const uint32_t l2 = rev ? (uint32_t)rev[r.link] : r.link;
-    const unsigned long long t0 = T_rs - (r.t_start + w[r.link]);
+    const uint32_t l2 = (mirror && rev) ? (uint32_t)rev[r.link] : r.link;
+    const unsigned long long t0 = mirror ? T_rs - (r.t_start + w[r.link]) : r.t_start;
     keys[i] = (t0 << lbits) | l2;
     vals[i] = (uint32_t)i;
   }
@@ -241,17 +244,22 @@ __global__ void rs_keys_kernel(const Rec *__restrict__ rec, uint64_t M, const ui
 __global__ void rs_emit_kernel(const uint32_t *__restrict__ vals, const Rec *__restrict__ rec, uint64_t M,
                                const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                                const uint32_t *__restrict__ w, const int32_t *__restrict__ rev, uint64_t T_rs,
-                               Send32 *__restrict__ out) {
+                               uint32_t mirror, uint64_t shift, Send32 *__restrict__ out) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < M; j += (uint64_t)gridDim.x * blockDim.x) {
     const Rec r = rec[vals[j]];
-    const uint32_t l2 = rev ? (uint32_t)rev[r.link] : r.link;
+    const uint32_t l2 = (mirror && rev) ? (uint32_t)rev[r.link] : r.link;
     Send32 s;
     s.chunk = r.chunk;
     s.link = l2;
     s.src = src[l2];
     s.dst = dst[l2];
-    s.t0 = T_rs - (r.t_start + w[r.link]);
-    s.t1 = T_rs - r.t_start;
+    if (mirror) {
+      s.t0 = T_rs - (r.t_start + w[r.link]);
+      s.t1 = T_rs - r.t_start;
+    } else {  // records in arbitrary order (paper-literal variant): sorted, shifted AG sends
+      s.t0 = r.t_start + shift;
+      s.t1 = r.t_start + w[r.link] + shift;
+    }
     out[j] = s;
   }
 }
@@ -379,7 +387,7 @@ size_t rs_sort_scratch_bytes(uint64_t M) {
 
 int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
                         const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
-                        size_t scratch_bytes, uint32_t *launches, void *stream) {
+                        size_t scratch_bytes, uint32_t *launches, void *stream, uint32_t mirror, uint64_t shift) {
   cudaStream_t st = (cudaStream_t)stream;
   if (M == 0) return 0;
   if (scratch_bytes < rs_sort_scratch_bytes(M)) {
@@ -405,7 +413,7 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
     return -6;
   }
   uint32_t nl = 0;
-  rs_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(rec, M, w, rev, T_rs, lbits, ka, va);
+  rs_keys_kernel<<<grid_for(M, 256), 256, 0, st>>>(rec, M, w, rev, T_rs, lbits, mirror, ka, va);
   ++nl;
   int rc = check_launch("rs_keys_kernel");
   if (rc) return rc;
@@ -420,7 +428,7 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
     unsigned long long *tk = ka; ka = kb; kb = tk;
     uint32_t *tv = va; va = vb; vb = tv;
   }
-  rs_emit_kernel<<<grid_for(M, 256), 256, 0, st>>>(va, rec, M, src, dst, w, rev, T_rs,
+  rs_emit_kernel<<<grid_for(M, 256), 256, 0, st>>>(va, rec, M, src, dst, w, rev, T_rs, mirror, shift,
                                                    reinterpret_cast<Send32 *>(out_sends));
   ++nl;
   if (launches) *launches += nl;

@@ -276,3 +276,39 @@ def test_table_iv_faulty_mesh(T):
     topo = W.Topology(n2, src, dst, al, bw)
     syn, sch, _ = run_both(T, topo, 1, 1 << 20, "AR", 16)
     assert_parity(syn, sch, "AR")
+
+
+def oracle_literal_stats(syn):
+    runs = list(syn.ag) + (list(syn.rs) if syn.rs is not syn.ag else [])
+    return sum(r.X for r in runs)
+
+
+@pytest.mark.parametrize("name", ["torus44_k2", "mesh6_hetero_k2", "config5", "rand_asym", "config3"])
+def test_literal_variant_parity(T, name):
+    """Row f1: the paper-literal chunk-first variant with chunk replacement on the
+    GPU vs oracle_greedy_literal, bit-exact (schedule, per-seed times, counters,
+    cancellations)."""
+    topo, k, coll, seeds = {
+        "torus44_k2": (W.torus([4, 4]), 2, "AR", 8),
+        "mesh6_hetero_k2": (W.mesh2d(6, 6, 200, 100), 2, "AR", 8),
+        "config5": (W.config(5).topo, 1, "AR", 16),
+        "rand_asym": (W.random_strongly_connected(9, 20, 5, bws=(25, 50, 100), alphas=(0, 500)), 2, "AR", 6),
+        "config3": (W.config(3).topo, 1, "AG", 4),
+    }[name]
+    syn = oracle.synthesize(topo, k, 1 << 20, coll, list(range(seeds)), literal=True)
+    t = T.Topology.from_workload_topology(topo)
+    sch = T.synthesize(t, coll, k, 1 << 20, seeds, keep_seed_times=True, literal=True)
+    assert_parity(syn, sch, coll)
+    assert sch.result["cancelled"] == oracle_literal_stats(syn)
+
+
+def test_literal_custom_replacement(T):
+    topo = W.Topology(3, np.array([0, 0, 1], np.int32), np.array([2, 1, 2], np.int32),
+                      np.array([2, 0, 0], np.uint32), np.array([2**31] * 3, np.uint32))
+    pre = oracle.bits_from_sets(3, 1, {0: [0]})
+    post = oracle.bits_from_sets(3, 1, {0: [0], 1: [0], 2: [0]})
+    syn = oracle.synthesize(topo, 1, 1, "CUSTOM", list(range(8)), pre=pre, post=post, n_chunks=1, literal=True)
+    t = T.Topology.from_workload_topology(topo)
+    sch = T.synthesize(t, "CUSTOM", 1, 1, 8, keep_seed_times=True, pre=pre, post=post, n_chunks=1, literal=True)
+    assert sch.result["T"] == 2 and sch.result["cancelled"] == 8
+    assert_parity(syn, sch, "CUSTOM")

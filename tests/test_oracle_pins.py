@@ -456,3 +456,80 @@ def test_bruteforce_self_check():
     assert optimum(3, [(a, b, 1) for a in range(3) for b in range(3) if a != b], *allgather_masks(3, 1)) == 1
     assert optimum(3, [(0, 1, 2), (1, 0, 2), (1, 2, 2), (2, 1, 2)], *allgather_masks(3, 1)) == 4
     assert optimum(2, [(0, 1, 1), (1, 0, 1)], *allgather_masks(2, 2)) == 2
+
+
+# --------------------------------------------------------------------------
+# Paper-literal variant (row f1, reading R21): chunk-first + replacement
+# --------------------------------------------------------------------------
+def _custom_literal(n, links, C, pre, post, seeds=range(16)):
+    src = np.array([l[0] for l in links], np.int32)
+    dst = np.array([l[1] for l in links], np.int32)
+    w = np.array([l[2] for l in links], np.uint64)
+    preb = oracle.bits_from_sets(n, C, pre)
+    postb = oracle.bits_from_sets(n, C, post)
+    return [oracle.greedy(n, src, dst, w, C, 1, s, 0, preb, postb, literal=True) for s in seeds]
+
+
+def test_literal_replacement_fig_heterogeneous_c():
+    """Fig. HeterogeneousGreedy(c): the chunk requested at t=0 over the
+    slow link 0->2 (w=3) is requested again at t=1 over 1->2 once NPU 1 holds it;
+    it arrives at t=2 and the copy still on 0->2 is outdated and cancelled.
+    Every seed: T = 2, sends {(c0, 0->1, 0, 1), (c0, 1->2, 1, 2)}, one cancellation.
+    (Link-first with persistent claims gives T = 3 on the same instance, E7.)"""
+    for r in _custom_literal(3, [(0, 2, 3), (0, 1, 1), (1, 2, 1)], 1, {0: [0]}, {0: [0], 1: [0], 2: [0]}):
+        assert _tuples(r) == [(0, 0, 1, 0, 1), (0, 1, 2, 1, 2)]
+        assert r.T == 2 and r.X == 1 and r.M == 3
+
+
+def test_literal_shorter_first_and_arrival_time():
+    """E5 and E6 hold for the literal variant too."""
+    for r in _custom_literal(3, [(1, 2, 2), (0, 2, 1)], 1, {0: [0], 1: [0]}, {0: [0], 1: [0], 2: [0]}):
+        assert _tuples(r) == [(0, 0, 2, 0, 1)] and r.T == 1
+    for r in _custom_literal(3, [(2, 1, 2), (1, 0, 1)], 1, {2: [0]}, {0: [0], 1: [0], 2: [0]}):
+        assert _tuples(r) == [(0, 1, 0, 2, 3), (0, 2, 1, 0, 2)] and r.T == 3
+
+
+@pytest.mark.parametrize("p", [3, 4, 7])
+def test_literal_closed_forms(p):
+    """Uni ring (p-1)w, bi ring ceil((p-1)/2)w, FC w: unique frontiers, so the
+    literal variant matches the closed forms (and never cancels)."""
+    for topo, want in ((W.uni_ring(p), (p - 1)), (W.bi_ring(p), (p - 1 + 1) // 2), (W.fully_connected(p), 1)):
+        w = oracle.link_costs(topo, 1 << 20)
+        for seed in range(4):
+            r = oracle.greedy(p, topo.src, topo.dst, w, p, 1, seed, literal=True)
+            assert r.T == want * int(w[0]) and r.X == 0
+
+
+@pytest.mark.parametrize("name", ["torus44", "mesh34_hetero", "rand7", "hybrid"])
+def test_literal_invariants(name):
+    """The final literal schedule is a valid congestion-free AG: exactly-once
+    delivery, arrival before departure, durations, disjoint link intervals;
+    issued = delivered + cancelled."""
+    topo = {
+        "torus44": W.torus([4, 4]),
+        "mesh34_hetero": W.mesh2d(3, 4, 200, 100),
+        "rand7": W.random_strongly_connected(7, 20, 11, bws=(25, 50, 100), alphas=(0, 500, 1500)),
+        "hybrid": W.remove_undirected_links(W.switch_hypercube_hybrid(4, 4, 20, 25), 0.05, 1)[0],
+    }[name]
+    k = 2
+    w = oracle.link_costs(topo, 256 << 10)
+    for seed in range(6):
+        r = oracle.greedy(topo.n_npus, topo.src, topo.dst, w, topo.n_npus * k, k, seed, literal=True)
+        rep = check(topo.n_npus, topo.src, topo.dst, w, r.sends, *ag_sets(topo.n_npus, k), greedy=False)
+        assert clean(rep), rep
+        assert rep["T"] == r.T
+        assert len(r.sends) == topo.n_npus * k * (topo.n_npus - 1) == r.M - r.X
+
+
+@pytest.mark.parametrize("inst", range(8))
+def test_literal_never_beats_exhaustive_optimum(inst):
+    rng = np.random.default_rng(2000 + inst)
+    n = int(rng.integers(2, 5))
+    L = int(rng.integers(n, min(6, n * (n - 1)) + 1))
+    topo = W.random_strongly_connected(n, L, 2000 + inst)
+    w = rng.integers(1, 4, size=topo.n_links).astype(np.uint64)
+    links = [(int(s), int(d), int(x)) for s, d, x in zip(topo.src, topo.dst, w)]
+    t_opt = optimum(n, links, *allgather_masks(n, 1))
+    for seed in range(8):
+        r = oracle.greedy(n, topo.src, topo.dst, w, n, 1, seed, literal=True)
+        assert r.T >= t_opt
