@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="tacos", choices=["tacos", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="steps of the end-to-end leg (default = steps)")
+    ap.add_argument("--literal", action="store_true", help="paper-literal chunk-first variant (row f1)")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the continuous-time Ring/Direct comparison")
     return ap.parse_args()
 
 
@@ -232,7 +234,7 @@ def run_gpu(args):
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     topo = T.Topology.from_workload_topology(wl.topo)
-    plan = T.Plan(topo, wl.collective, wl.chunks_per_npu, wl.chunk_bytes, S, 0, rank * S)
+    plan = T.Plan(topo, wl.collective, wl.chunks_per_npu, wl.chunk_bytes, S, 0, rank * S, literal=args.literal)
     n_sends = plan.n_sends
     d_sends = torch.empty(n_sends * 32, dtype=torch.uint8, device="cuda")
     keys = plan.best_keys_tensor()
@@ -315,7 +317,8 @@ def run_gpu(args):
     h2d = wl.topo.n_links * 16
     d2h = 0
     e2e_ms = []
-    p_e2e, keep = T.make_params(wl.collective, wl.chunks_per_npu, wl.chunk_bytes, S, 0, rank * S)
+    p_e2e, keep = T.make_params(wl.collective, wl.chunks_per_npu, wl.chunk_bytes, S, 0, rank * S,
+                                flags=T.TACOS_FLAG_LITERAL if args.literal else 0)
     for i in range(1 + e2e_steps):
         barrier()
         t0 = time.perf_counter()
@@ -342,6 +345,24 @@ def run_gpu(args):
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = m_total * len(e2e_ms) / (float(e2e_t[0]) / 1e3)
+
+    # continuous-time collective time of the winning schedule vs the Ring / Direct
+    # baselines (row f3): the paper's normalized comparison
+    coll_times = None
+    if rank == 0 and not args.no_baselines and world == 1:
+        sends_h = T.sends_from_bytes(host_out.numpy())
+        tac = T.evaluate_continuous(topo, sends_h, wl.collective, wl.chunks_per_npu, wl.chunk_bytes)["T_ns"]
+        coll_times = {"tacos_us": tac / 1e3}
+        n = wl.topo.n_npus
+        for alg in ("ring", "direct"):
+            est = n * (n - 1) * wl.chunks_per_npu * (8 if alg == "direct" else 2)
+            if est > 40_000_000:  # the baseline schedule alone would need several GB of host memory
+                coll_times[alg + "_us"] = None
+                continue
+            bs = T.baseline(topo, alg, wl.collective, wl.chunks_per_npu, wl.chunk_bytes)
+            coll_times[alg + "_us"] = T.evaluate_continuous(topo, bs, wl.collective, wl.chunks_per_npu,
+                                                            wl.chunk_bytes)["T_ns"] / 1e3
+            coll_times["speedup_vs_" + alg] = coll_times[alg + "_us"] / coll_times["tacos_us"]
 
     if rank == 0:
         cpu = None
@@ -370,7 +391,10 @@ def run_gpu(args):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"],
                        "samples": clk["samples"]},
-            "stats": {"V": stats["visits"], "D": stats["dest_events"], "M": stats["matches"], "E": stats["events"]},
+            "stats": {"V": stats["visits"], "D": stats["dest_events"], "M": stats["matches"], "E": stats["events"],
+                      "cancelled": stats.get("cancelled", 0)},
+            "variant": "paper-literal chunk-first + replacement (f1)" if args.literal else "link-first (R1, R4)",
+            "collective_time": coll_times,
             "wall_s": wall,
         }
         print(json.dumps(line), flush=True)

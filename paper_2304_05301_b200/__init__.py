@@ -442,9 +442,9 @@ class Plan:
     best keys across ranks (caller), emit on the owning rank."""
 
     def __init__(self, topo: Topology, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=1,
-                 base_seed=0, seed_offset=0, time_unit_ns=1, no_schedule=False):
+                 base_seed=0, seed_offset=0, time_unit_ns=1, no_schedule=False, literal=False):
         self.topo = topo
-        flags = TACOS_FLAG_NO_SCHEDULE if no_schedule else 0
+        flags = (TACOS_FLAG_NO_SCHEDULE if no_schedule else 0) | (TACOS_FLAG_LITERAL if literal else 0)
         self.params, self._keep = make_params(collective, chunks_per_npu, chunk_bytes, n_seeds, base_seed, seed_offset,
                                               time_unit_ns, flags)
         h = ctypes.c_void_p()
