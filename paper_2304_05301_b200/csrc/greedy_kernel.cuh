@@ -100,6 +100,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *bitmap2 = reinterpret_cast<uint32_t *>(smem + lay.off_bitmap);  // 2 x nbw words (event parity)
   uint32_t *wpre = reinterpret_cast<uint32_t *>(smem + lay.off_wpre);
   uint32_t *s_inptr = reinterpret_cast<uint32_t *>(smem + lay.off_inptr);  // CSR offsets, own range
+  uint32_t *s_act = reinterpret_cast<uint32_t *>(smem + lay.off_act);      // worklist bitmaps (2 x act_words)
+  uint32_t *s_list = reinterpret_cast<uint32_t *>(smem + lay.off_list);    // worklist entries
+  __shared__ uint32_t s_nwork;
   const uint32_t nbw = (L + 31u) / 32u;
   const uint32_t seed_lo = (uint32_t)job.seed, seed_hi = (uint32_t)(job.seed >> 32);
   Rec *rec = job.rec;
@@ -108,6 +111,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t chunkN = (N + Q - 1u) / Q;
   const uint32_t d_lo = min(N, crank * chunkN), d_hi = min(N, d_lo + chunkN);
   const uint32_t p_lo = __ldg(&in_ptr[d_lo]), p_hi = __ldg(&in_ptr[d_hi]);
+  const uint32_t act_words = (d_hi - d_lo + 31u) / 32u;
+  const bool worklist = lay.worklist != 0u;
   auto cluster_barrier = [&]() {
     if (Q > 1) cluster.sync();
     else __syncthreads();
@@ -147,6 +152,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) hver[x] = 0u;
   for (uint32_t x = d_lo + tid; x <= d_hi; x += nthr) s_inptr[x] = __ldg(&in_ptr[x]);
   for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
+  if (worklist)
+    for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;
   if (tid == 0) {
     s_delivered = 0ull;
     s_V = s_D = s_M = 0ull;
@@ -251,12 +258,56 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     if (tid == 0) s_rec_base = s_next_base;
     ++E;
 
+    // ================= PW (optional): worklist of destinations with a live in-link =================
+    // For sparse events (heterogeneous costs free few links per event) the destination
+    // phase then visits only the destinations that can match; V and D are counted here.
+    uint32_t n_work = d_hi - d_lo;
+    if (worklist) {
+      uint32_t *act = s_act;                    // bit i: own destination d_lo + i has a live in-link
+      uint32_t *anyf = s_act + act_words;       // bit i: ... has a free in-link
+      uint32_t nfree = 0;
+      for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
+        if (busy[q] > t) continue;
+        ++nfree;
+        const uint32_t i = __ldg(&T.p_dst[q]) - d_lo;
+        atomicOr(&anyf[i >> 5], 1u << (i & 31u));
+        if (seen[q] != hver_of(t_src[q])) atomicOr(&act[i >> 5], 1u << (i & 31u));
+      }
+      myV += nfree;
+      __syncthreads();
+      if (tid < 32) {  // compact the active destinations (ascending id), count D
+        uint32_t running = 0, nd = 0;
+        for (uint32_t base = 0; base < act_words; base += 32u) {
+          const uint32_t i = base + lane;
+          const uint32_t a = i < act_words ? act[i] : 0u;
+          nd += i < act_words ? __popc(anyf[i]) : 0u;
+          const uint32_t c = __popc(a);
+          uint32_t incl = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+          }
+          uint32_t pos = running + incl - c;
+          for (uint32_t bits = a; bits; bits &= bits - 1u) s_list[pos++] = d_lo + i * 32u + (__ffs(bits) - 1u);
+          running += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        nd = __reduce_add_sync(0xFFFFFFFFu, nd);
+        if (lane == 0) {
+          s_nwork = running;
+          myD += nd;
+        }
+      }
+      __syncthreads();
+      n_work = s_nwork;
+    }
     if (tracing) ts[3] = clock64();
 
     // ================= PM: per-destination draws, order and matching =================
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
-      for (uint32_t d = d_lo + tid / P; d < d_hi; d += ngroups) {
+      for (uint32_t wi = tid / P; wi < n_work; wi += ngroups) {
+        const uint32_t d = worklist ? s_list[wi] : d_lo + wi;
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         const uint32_t deg = b1 - b0;
         uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
@@ -412,7 +463,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             nfree = __reduce_add_sync(gmask, nfree);
             nlive = __reduce_add_sync(gmask, nlive);
           }
-          if (gl == 0) {
+          if (gl == 0 && !worklist) {
             myV += nfree;
             myD += nfree ? 1u : 0u;
           }
@@ -492,7 +543,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           nfree = __reduce_add_sync(gmask, nfree);
           nl = __reduce_add_sync(gmask, nl);
         }
-        if (gl == 0) {
+        if (gl == 0 && !worklist) {
           myV += nfree;
           myD += nfree ? 1u : 0u;
         }
@@ -573,6 +624,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         if (lane == 0) s_next_base = s_rec_base + running;
       }
       for (uint32_t i = tid; i < nbw; i += nthr) bm_clear[i] = 0u;
+      if (worklist)
+        for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;  // consumed by this event's PM
     }
     unsigned long long tn = s_min;
     if (Q > 1)

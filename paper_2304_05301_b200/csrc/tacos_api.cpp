@@ -528,6 +528,18 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       g.lay.cluster = 1;
     }
     if (const char *env = getenv("TACOS_REG_PATH")) g.lay.reg_path = (uint32_t)atoi(env);
+    // worklist for sparse events: several distinct link costs free only some links per event
+    bool multi_w = false;
+    for (size_t gk = gi; gk < gj && !multi_w; ++gk) {
+      const auto &wv = pl->parts[order[gk]].w;
+      for (size_t l = 1; l < wv.size(); ++l)
+        if (wv[l] != wv[0]) {
+          multi_w = true;
+          break;
+        }
+    }
+    g.lay.worklist = multi_w ? 1u : 0u;
+    if (const char *env = getenv("TACOS_WORKLIST")) g.lay.worklist = (uint32_t)atoi(env);
     g.job_begin = begin;
     g.job_end = n_jobs;
     pl->groups.push_back(g);

@@ -69,13 +69,14 @@ struct Layout {
   uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv;
   uint32_t off_tsrc, off_tw, off_tlid;  // per-position topology copies (src, w, link id)
   // always in shared memory, after [rows][links] when those are resident
-  uint32_t off_hver, off_bitmap, off_wpre, off_inptr;  // bitmap: 2 x ceil(L/32) words (event parity)
+  uint32_t off_hver, off_bitmap, off_wpre, off_inptr, off_act, off_list;  // bitmap: 2 x ceil(L/32) words (event parity)
   uint32_t smem_bytes;   // total dynamic smem
   uint32_t rows_in_smem, links_in_smem;
   uint32_t threads;
   uint32_t pre_draw;     // 1: draws per position by all threads before the destination phase
   uint32_t cluster;      // CTAs per job (thread-block cluster size), 1 = one CTA per job
   uint32_t reg_path;     // 1: every in-degree <= 8 (register ranking path)
+  uint32_t worklist;     // 1: compact the destinations with a live in-link before matching
 };
 
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,
