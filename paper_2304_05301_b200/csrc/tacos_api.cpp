@@ -538,7 +538,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
           break;
         }
     }
-    g.lay.worklist = multi_w ? 1u : 0u;
+    g.lay.worklist = (multi_w && g.lay.reg_path) ? 1u : 0u;  // measured: helps the mesh (config 4), not config 5
     if (const char *env = getenv("TACOS_WORKLIST")) g.lay.worklist = (uint32_t)atoi(env);
     g.job_begin = begin;
     g.job_end = n_jobs;
