@@ -73,6 +73,11 @@ def lib():
             l.oracle_greedy.restype = ctypes.c_int
             l.oracle_greedy_literal.argtypes = l.oracle_greedy.argtypes
             l.oracle_greedy_literal.restype = ctypes.c_int
+            l.oracle_greedy_relay.argtypes = [
+                ctypes.c_int32, ctypes.c_int32, i32p, i32p, u64p, ctypes.c_uint32, u32p, u32p, u32p,
+                ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64, u64p, u64p, u64p,
+            ]
+            l.oracle_greedy_relay.restype = ctypes.c_int
             _lib = l
     return _lib
 
@@ -132,9 +137,11 @@ class GreedyResult:
 
 def greedy(n_npus: int, src: np.ndarray, dst: np.ndarray, w: np.ndarray, n_chunks: int, k: int, seed: int,
            sigma: int = 0, pre: Optional[np.ndarray] = None, post: Optional[np.ndarray] = None,
-           record: bool = True, literal: bool = False) -> GreedyResult:
+           record: bool = True, literal: bool = False, allow: Optional[np.ndarray] = None) -> GreedyResult:
     """One TACOS-Greedy synthesis (SURVEY §8(c) pseudo-code); literal=True runs the
-    paper-literal chunk-first variant with chunk replacement (row f1, reading R21)."""
+    paper-literal chunk-first variant with chunk replacement (row f1, reading R21);
+    allow (L x ceil(C/32) words, CUSTOM only) = the chunks each link may carry,
+    relays included (row f2, reading R22; see oracle/collectives.py)."""
     src = np.ascontiguousarray(src, dtype=np.int32)
     dst = np.ascontiguousarray(dst, dtype=np.int32)
     w = np.ascontiguousarray(w, dtype=np.uint64)
@@ -146,17 +153,30 @@ def greedy(n_npus: int, src: np.ndarray, dst: np.ndarray, w: np.ndarray, n_chunk
         pre = np.ascontiguousarray(pre, dtype=np.uint32).reshape(n_npus, Wd)
         post = np.ascontiguousarray(post, dtype=np.uint32).reshape(n_npus, Wd)
         cap = int(sum(bin(int(x)).count("1") for x in (post & ~pre).ravel()))
+        if allow is not None:  # relays: every (NPU, chunk) pair is delivered at most once
+            cap = n_npus * n_chunks - int(sum(bin(int(x)).count("1") for x in pre.ravel()))
         pre_p, post_p = _p(pre, ctypes.c_uint32), _p(post, ctypes.c_uint32)
     sends = np.zeros(max(cap, 1), dtype=SEND_DTYPE)
     n_sends = ctypes.c_uint64(0)
     T = ctypes.c_uint64(0)
     stats = np.zeros(5, dtype=np.uint64)
-    fn = lib().oracle_greedy_literal if literal else lib().oracle_greedy
-    rc = fn(
-        n_npus, src.shape[0], _p(src, ctypes.c_int32), _p(dst, ctypes.c_int32), _p(w, ctypes.c_uint64),
-        n_chunks, k, pre_p, post_p, ctypes.c_uint64(seed & (2**64 - 1)), sigma,
-        sends.ctypes.data if record else None, cap, ctypes.byref(n_sends), ctypes.byref(T), _p(stats, ctypes.c_uint64),
-    )
+    if allow is not None:
+        if pre is None or literal:
+            raise ValueError("allow masks need CUSTOM pre/post and the link-first variant")
+        allow = np.ascontiguousarray(allow, dtype=np.uint32).reshape(src.shape[0], Wd)
+        rc = lib().oracle_greedy_relay(
+            n_npus, src.shape[0], _p(src, ctypes.c_int32), _p(dst, ctypes.c_int32), _p(w, ctypes.c_uint64),
+            n_chunks, pre_p, post_p, _p(allow, ctypes.c_uint32), ctypes.c_uint64(seed & (2**64 - 1)), sigma,
+            sends.ctypes.data if record else None, cap, ctypes.byref(n_sends), ctypes.byref(T),
+            _p(stats, ctypes.c_uint64))
+    else:
+        fn = lib().oracle_greedy_literal if literal else lib().oracle_greedy
+        rc = fn(
+            n_npus, src.shape[0], _p(src, ctypes.c_int32), _p(dst, ctypes.c_int32), _p(w, ctypes.c_uint64),
+            n_chunks, k, pre_p, post_p, ctypes.c_uint64(seed & (2**64 - 1)), sigma,
+            sends.ctypes.data if record else None, cap, ctypes.byref(n_sends), ctypes.byref(T),
+            _p(stats, ctypes.c_uint64),
+        )
     if rc != OK:
         raise OracleError(rc, f"greedy seed={seed} sigma={sigma}")
     return GreedyResult(int(T.value), sends[: int(n_sends.value)] if record else sends[:0], int(stats[0]),
@@ -215,32 +235,51 @@ class Synthesis:
     rs: List[GreedyResult]
 
 
+NAMED = ("BROADCAST", "REDUCE", "SCATTER", "GATHER")
+
+
 def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "AR", seeds: Sequence[int] = (0,),
                time_unit_ns: int = 1, pre: Optional[np.ndarray] = None, post: Optional[np.ndarray] = None,
                threads: Optional[int] = None, record: bool = True, n_chunks: Optional[int] = None,
-               literal: bool = False) -> Synthesis:
+               literal: bool = False, relay: bool = False, root: int = 0) -> Synthesis:
     """Best-of-S TACOS-Greedy synthesis of AG / RS / AR (or CUSTOM with pre/post,
-    collective 'CUSTOM').  seeds are the 64-bit Philox keys; ties go to the
-    lowest position in ``seeds`` (R11)."""
+    collective 'CUSTOM', relays with relay=True), or of the named collectives of
+    row f2: BROADCAST / SCATTER searched forward (Scatter with relays), REDUCE /
+    GATHER as the inverse of BROADCAST / SCATTER on G^T, k chunks per
+    NPU, `root`.  seeds are the 64-bit Philox keys; ties go to the lowest
+    position in ``seeds`` (R11)."""
+    from . import collectives as _coll
+
     n = topo.n_npus
     w = link_costs(topo, chunk_bytes, time_unit_ns)
-    if pre is None:
+    if collective in NAMED:
+        fwd = collective if collective in ("BROADCAST", "SCATTER") else _coll.dual(collective)
+        C, pre, post = _coll.named_bits(fwd, n, chunks_per_npu, root)
+        relay = relay or fwd == "SCATTER"
+    elif pre is None:
         C = n * chunks_per_npu
     else:
         if n_chunks is None:
             raise ValueError("CUSTOM pre/post needs n_chunks")
         C = int(n_chunks)
+    if relay and pre is None:
+        raise ValueError("relays need a CUSTOM or named collective")
     src, dst = topo.src, topo.dst
     threads = threads or min(len(seeds), os.cpu_count() or 1)
 
     def run(args):
-        s, sig, a, b = args
-        return greedy(n, a, b, w, C, chunks_per_npu, s, sig, pre, post, record, literal)
+        s, sig, a, b, allow = args
+        return greedy(n, a, b, w, C, chunks_per_npu, s, sig, pre, post, record, literal, allow)
 
-    jobs_ag = [(s, 0, src, dst) for s in seeds]
     rev = reverse_links(src, dst, w)
-    need_rs = collective in ("RS", "AR")
-    jobs_rs = [] if (not need_rs or rev is not None) else [(s, 1, dst, src) for s in seeds]
+    need_rs = collective in ("RS", "AR", "REDUCE", "GATHER")
+    only_rs = collective in ("RS", "REDUCE", "GATHER")
+    rs_on_gt = need_rs and rev is None
+    allow0 = _coll.relay_allow(n, src, dst, C, pre, post) if relay else None
+    allow1 = _coll.relay_allow(n, dst, src, C, pre, post) if relay and rs_on_gt else None
+    # the forward runs (sigma 0) are made even when only the G^T phase is used, as by the library
+    jobs_ag = [(s, 0, src, dst, allow0) for s in seeds]
+    jobs_rs = [(s, 1, dst, src, allow1) for s in seeds] if rs_on_gt else []
     with ThreadPoolExecutor(max_workers=threads) as ex:
         res = list(ex.map(run, jobs_ag + jobs_rs))
     ag = res[: len(jobs_ag)]
@@ -248,7 +287,7 @@ def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "A
     T_ag = np.array([r.T for r in ag], dtype=np.uint64)
     T_rs = np.array([r.T for r in rs], dtype=np.uint64)
     i_ag = int(np.argmin(T_ag))  # argmin returns the first (lowest index) minimum
-    if collective == "AG" or collective == "CUSTOM":
+    if not need_rs:  # AG, CUSTOM, BROADCAST, SCATTER
         win = ag[i_ag]
         return Synthesis(collective, win.T, canonical(win.sends) if record else win.sends, seeds[i_ag], seeds[i_ag],
                          win.T, 0, T_ag, ag, [])
@@ -262,8 +301,8 @@ def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "A
     win_rs = rs[i_rs]
     T_RS = win_rs.T
     rs_sends = mirror(win_rs.sends, T_RS, src, dst, rev) if record else win_rs.sends[:0]
-    if collective == "RS":
-        return Synthesis("RS", T_RS, canonical(rs_sends), seeds[i_rs], seeds[i_rs], 0, T_RS, T_rs, ag, rs)
+    if only_rs:
+        return Synthesis(collective, T_RS, canonical(rs_sends), seeds[i_rs], seeds[i_rs], 0, T_RS, T_rs, ag, rs)
     win_ag = ag[i_ag]
     ag_sh = win_ag.sends.copy()
     ag_sh["t_start"] += np.uint64(T_RS)

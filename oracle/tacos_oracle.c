@@ -114,11 +114,20 @@ static int cmp_free_link(const void *pa, const void *pb) {
  * stats[0]=V free-link visits, [1]=D (destination,event) pairs with a free
  * in-link, [2]=M matches, [3]=E events at which matching ran.
  */
-int oracle_greedy(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst, const uint64_t *w,
-                  uint32_t n_chunks, uint32_t k, const uint32_t *pre_bits, const uint32_t *post_bits,
-                  uint64_t seed, uint32_t sigma, oracle_send *sends, uint64_t cap, uint64_t *n_sends_out,
-                  uint64_t *T_out, uint64_t *stats) {
+/*
+ * allow_bits (NULL, or CUSTOM only): L rows of ceil(C/32) words, row l = the
+ * chunks link l may carry (reading R22: post[dst]
+ * plus the chunks dst may relay).  The candidate set then reads allow[l]
+ * instead of post[d], and only arrivals of chunks in post[dst] count towards
+ * the postcondition (a relayed chunk is held, so it can be forwarded, but it
+ * is not required at the relay).
+ */
+static int greedy_impl(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst, const uint64_t *w,
+                       uint32_t n_chunks, uint32_t k, const uint32_t *pre_bits, const uint32_t *post_bits,
+                       const uint32_t *allow_bits, uint64_t seed, uint32_t sigma, oracle_send *sends, uint64_t cap,
+                       uint64_t *n_sends_out, uint64_t *T_out, uint64_t *stats) {
   if (n_npus < 1 || n_links < 0 || n_chunks < 1) return ORACLE_E_INVALID_ARG;
+  if (allow_bits != NULL && pre_bits == NULL) return ORACLE_E_INVALID_ARG;
   const uint32_t N = (uint32_t)n_npus, L = (uint32_t)n_links, C = n_chunks;
   const uint32_t W = (C + 31) / 32;
   int rc = ORACLE_OK;
@@ -186,7 +195,7 @@ int oracle_greedy(int32_t n_npus, int32_t n_links, const int32_t *src, const int
       if (cur[l] != NONE && busy_until[l] == t) {
         bit_set(&held[(size_t)dst[l] * W], cur[l]);
         bit_clr(&pending[(size_t)dst[l] * W], cur[l]);
-        delivered += 1;
+        if (bit_get(&post[(size_t)dst[l] * W], cur[l])) delivered += 1; /* a relay arrival is not required */
         cur[l] = NONE;
       }
     }
@@ -220,10 +229,11 @@ int oracle_greedy(int32_t n_npus, int32_t n_links, const int32_t *src, const int
         uint32_t l = F[i].link;
         const uint32_t *held_s = &held[(size_t)src[l] * W];
         V += 1;
-        /* cand = post[d] & held[src] & ~held[d] & ~claimed */
+        /* cand = post[d] & held[src] & ~held[d] & ~claimed  (allow[l] in place of post[d] with relays) */
+        const uint32_t *mask = allow_bits ? &allow_bits[(size_t)l * W] : post_d;
         uint64_t K = 0;
         for (uint32_t q = 0; q < W; ++q) {
-          cand[q] = post_d[q] & held_s[q] & ~held_d[q] & ~claimed[q];
+          cand[q] = mask[q] & held_s[q] & ~held_d[q] & ~claimed[q];
           K += (uint64_t)__builtin_popcount(cand[q]);
         }
         if (K == 0) continue;
@@ -267,6 +277,15 @@ int oracle_greedy(int32_t n_npus, int32_t n_links, const int32_t *src, const int
     if (t_next == UINT64_MAX) { rc = ORACLE_E_UNREACHABLE; *T_out = t; break; }
     t = t_next;
   }
+  /* Relays (R22): a send still in flight when the postcondition holds carries a
+   * chunk nobody requires any more (every required chunk has arrived); it leaves
+   * the schedule.  Without relays nothing is in flight at that point. */
+  if (rc == ORACLE_OK && sends) {
+    uint64_t kept = 0;
+    for (uint64_t i = 0; i < n_sends; ++i)
+      if (sends[i].t_end <= *T_out) sends[kept++] = sends[i];
+    n_sends = kept;
+  }
   *n_sends_out = n_sends;
   if (stats) { stats[0] = V; stats[1] = D; stats[2] = M; stats[3] = E; }
 
@@ -274,6 +293,24 @@ done:
   free(held); free(pending); free(post); free(claimed); free(cand);
   free(busy_until); free(cur); free(F); free(in_start); free(in_list);
   return rc;
+}
+
+int oracle_greedy(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst, const uint64_t *w,
+                  uint32_t n_chunks, uint32_t k, const uint32_t *pre_bits, const uint32_t *post_bits,
+                  uint64_t seed, uint32_t sigma, oracle_send *sends, uint64_t cap, uint64_t *n_sends_out,
+                  uint64_t *T_out, uint64_t *stats) {
+  return greedy_impl(n_npus, n_links, src, dst, w, n_chunks, k, pre_bits, post_bits, NULL, seed, sigma, sends, cap,
+                     n_sends_out, T_out, stats);
+}
+
+/* CUSTOM with a per-link allow mask (relays, R22); see greedy_impl. */
+int oracle_greedy_relay(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst, const uint64_t *w,
+                        uint32_t n_chunks, const uint32_t *pre_bits, const uint32_t *post_bits,
+                        const uint32_t *allow_bits, uint64_t seed, uint32_t sigma, oracle_send *sends, uint64_t cap,
+                        uint64_t *n_sends_out, uint64_t *T_out, uint64_t *stats) {
+  if (allow_bits == NULL) return ORACLE_E_INVALID_ARG;
+  return greedy_impl(n_npus, n_links, src, dst, w, n_chunks, 0, pre_bits, post_bits, allow_bits, seed, sigma, sends,
+                     cap, n_sends_out, T_out, stats);
 }
 
 /*

@@ -35,11 +35,17 @@ TACOS_ALL_GATHER = 0
 TACOS_REDUCE_SCATTER = 1
 TACOS_ALL_REDUCE = 2
 TACOS_CUSTOM = 3
-COLLECTIVES = {"AG": TACOS_ALL_GATHER, "RS": TACOS_REDUCE_SCATTER, "AR": TACOS_ALL_REDUCE, "CUSTOM": TACOS_CUSTOM}
+TACOS_BROADCAST = 4
+TACOS_REDUCE = 5
+TACOS_SCATTER = 6
+TACOS_GATHER = 7
+COLLECTIVES = {"AG": TACOS_ALL_GATHER, "RS": TACOS_REDUCE_SCATTER, "AR": TACOS_ALL_REDUCE, "CUSTOM": TACOS_CUSTOM,
+               "BROADCAST": TACOS_BROADCAST, "REDUCE": TACOS_REDUCE, "SCATTER": TACOS_SCATTER, "GATHER": TACOS_GATHER}
 
 TACOS_FLAG_NO_SCHEDULE = 1
 TACOS_FLAG_KEEP_SEED_TIMES = 2
 TACOS_FLAG_LITERAL = 4
+TACOS_FLAG_RELAY = 8
 
 VIOLATIONS = ("no_such_link", "wrong_duration", "link_overlap", "unheld_at_depart", "duplicate_delivery",
               "post_unmet", "phase_order")
@@ -61,7 +67,7 @@ class tacos_synth_params(ctypes.Structure):
                 ("time_unit_ns", ctypes.c_uint32), ("n_seeds", ctypes.c_uint32), ("base_seed", ctypes.c_uint64),
                 ("seed_offset", ctypes.c_uint32), ("n_chunks", ctypes.c_uint32),
                 ("pre_bits", ctypes.POINTER(ctypes.c_uint32)), ("post_bits", ctypes.POINTER(ctypes.c_uint32)),
-                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("root", ctypes.c_uint32)]
 
 
 class tacos_result(ctypes.Structure):
@@ -223,9 +229,10 @@ def tacos_free_topology(h):
 
 
 def make_params(collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=1, base_seed=0, seed_offset=0,
-                time_unit_ns=1, flags=0, pre=None, post=None, n_chunks=0) -> Tuple[tacos_synth_params, tuple]:
+                time_unit_ns=1, flags=0, pre=None, post=None, n_chunks=0, root=0) -> Tuple[tacos_synth_params, tuple]:
     """Build tacos_synth_params; returns (params, keepalive)."""
     p = tacos_synth_params()
+    p.root = root
     p.collective = COLLECTIVES[collective] if isinstance(collective, str) else int(collective)
     p.chunks_per_npu = chunks_per_npu
     p.chunk_bytes = chunk_bytes
@@ -375,11 +382,13 @@ class Schedule:
 
 def synthesize(topo: Topology, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=1, base_seed=0,
                time_unit_ns=1, keep_seed_times=False, no_schedule=False, pre=None, post=None,
-               n_chunks=0, literal=False) -> Schedule:
+               n_chunks=0, literal=False, relay=False, root=0) -> Schedule:
+    """tacos_synthesize.  collective: AG / RS / AR / CUSTOM (pre, post, n_chunks; relay=True
+    for relays, R22) or the rooted BROADCAST / REDUCE / SCATTER / GATHER (root)."""
     flags = ((TACOS_FLAG_KEEP_SEED_TIMES if keep_seed_times else 0) | (TACOS_FLAG_NO_SCHEDULE if no_schedule else 0)
-             | (TACOS_FLAG_LITERAL if literal else 0))
+             | (TACOS_FLAG_LITERAL if literal else 0) | (TACOS_FLAG_RELAY if relay else 0))
     p, keep = make_params(collective, chunks_per_npu, chunk_bytes, n_seeds, base_seed, 0, time_unit_ns, flags, pre,
-                          post, n_chunks)
+                          post, n_chunks, root)
     h = tacos_synthesize(topo.handle, p)
     try:
         sends = tacos_schedule_sends(h)
@@ -424,8 +433,8 @@ def synthesize_into(topo: Topology, params: tacos_synth_params, sends_ptr: int, 
 
 
 def evaluate(topo: Topology, sends: np.ndarray, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20,
-             time_unit_ns=1, pre=None, post=None, n_chunks=0) -> dict:
-    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1, 0, 0, time_unit_ns, 0, pre, post, n_chunks)
+             time_unit_ns=1, pre=None, post=None, n_chunks=0, root=0) -> dict:
+    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1, 0, 0, time_unit_ns, 0, pre, post, n_chunks, root)
     return tacos_eval(topo.handle, p, sends)
 
 
@@ -442,11 +451,13 @@ class Plan:
     best keys across ranks (caller), emit on the owning rank."""
 
     def __init__(self, topo: Topology, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=1,
-                 base_seed=0, seed_offset=0, time_unit_ns=1, no_schedule=False, literal=False):
+                 base_seed=0, seed_offset=0, time_unit_ns=1, no_schedule=False, literal=False, root=0,
+                 pre=None, post=None, n_chunks=0, relay=False):
         self.topo = topo
-        flags = (TACOS_FLAG_NO_SCHEDULE if no_schedule else 0) | (TACOS_FLAG_LITERAL if literal else 0)
+        flags = ((TACOS_FLAG_NO_SCHEDULE if no_schedule else 0) | (TACOS_FLAG_LITERAL if literal else 0)
+                 | (TACOS_FLAG_RELAY if relay else 0))
         self.params, self._keep = make_params(collective, chunks_per_npu, chunk_bytes, n_seeds, base_seed, seed_offset,
-                                              time_unit_ns, flags)
+                                              time_unit_ns, flags, pre, post, n_chunks, root)
         h = ctypes.c_void_p()
         _check(load_library().tacos_plan_create(topo.handle, ctypes.byref(self.params), ctypes.byref(h)),
                "tacos_plan_create")
@@ -553,8 +564,8 @@ def tacos_remove_npus(n_npus, src, dst, alpha_ns, bw, removed):
 # continuous-time evaluation and baselines (f3)
 # --------------------------------------------------------------------------
 def evaluate_continuous(topo: Topology, sends: np.ndarray, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20,
-                        pre=None, post=None, n_chunks=0) -> dict:
-    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1, 0, 0, 1, 0, pre, post, n_chunks)
+                        pre=None, post=None, n_chunks=0, root=0) -> dict:
+    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1, 0, 0, 1, 0, pre, post, n_chunks, root)
     rep = tacos_cont_report()
     s_ = np.ascontiguousarray(sends, dtype=SEND_DTYPE)
     _check(load_library().tacos_eval_continuous(topo.handle, ctypes.byref(p), s_.ctypes.data, s_.shape[0],
@@ -572,3 +583,55 @@ def baseline(topo: Topology, algorithm="ring", collective="AR", chunks_per_npu=1
     _check(lib.tacos_baseline(topo.handle, ctypes.byref(p), alg, out.ctypes.data, n.value, ctypes.byref(n)),
            "tacos_baseline")
     return out[: n.value]
+
+
+# --------------------------------------------------------------------------
+# multi-tenant collectives (Table VI)
+# --------------------------------------------------------------------------
+def multi_tenant(n_npus: int, tenants) -> Tuple[int, np.ndarray, np.ndarray, list]:
+    """Merge concurrent tenants into one CUSTOM pre/postcondition over disjoint
+    chunk ranges, to be synthesized with relay=True.  tenants: (kind, root, k)
+    with kind AG (root unused), BROADCAST, SCATTER, GATHER or REDUCE; a Reduce
+    tenant inside the merged forward search is scheduled as the Gather of its N
+    partial chunks (reading R23).  Returns (C, pre, post, first chunk
+    id of each tenant); pre/post are N x ceil(C/32) uint32 rows."""
+    n = int(n_npus)
+    spans = []
+    for kind, root, k in tenants:
+        if kind not in ("AG", "BROADCAST", "SCATTER", "GATHER", "REDUCE"):
+            raise ValueError(f"unknown tenant kind {kind}")
+        if kind != "AG" and not 0 <= root < n:
+            raise ValueError("tenant root out of range")
+        spans.append(k if kind == "BROADCAST" else n * k)
+    C = int(sum(spans))
+    words = (C + 31) // 32
+    held = np.zeros((n, C), dtype=bool)
+    need = np.zeros((n, C), dtype=bool)
+    first, base = [], 0
+    for (kind, root, k), span in zip(tenants, spans):
+        first.append(base)
+        ids = np.arange(base, base + span)
+        owner = (ids - base) // k
+        if kind == "AG":
+            held[owner, ids] = True
+            need[:, ids] = True
+        elif kind == "BROADCAST":
+            held[root, ids] = True
+            need[:, ids] = True
+        elif kind == "SCATTER":
+            held[root, ids] = True
+            need[root, ids] = True
+            need[owner, ids] = True
+        else:  # GATHER, REDUCE (R23)
+            held[owner, ids] = True
+            need[owner, ids] = True
+            need[root, ids] = True
+        base += span
+
+    def pack(m):
+        out = np.zeros((n, words), dtype=np.uint32)
+        for c in range(C):
+            out[:, c >> 5] |= (m[:, c].astype(np.uint32) << np.uint32(c & 31))
+        return out
+
+    return C, pack(held), pack(need), first

@@ -45,7 +45,9 @@ struct ThreadsFor {
   static constexpr int value = V > 1 ? 512 : 768;  // registers: <= 128 resp. <= 85 per thread
 };
 
-template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM, bool REG_PATH>
+// MASKED (relays, R22): candidates are also and-ed with the
+// per-position allow row, and only arrivals of chunks in post[dst] count.
+template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM, bool REG_PATH, bool MASKED>
 __global__ void __launch_bounds__(ThreadsFor<V>::value, 1)
 greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Layout lay) {
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
@@ -90,11 +92,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *order = reinterpret_cast<uint32_t *>(links_base + lay.off_order);
   unsigned char *lv = links_base + lay.off_lv;
   // per-position topology (source, cost, link id): staged into shared memory with the link state
-  const uint32_t *t_src = p_src, *t_w = p_w, *t_lid = p_lid;
+  const uint32_t *t_src = p_src, *t_w = p_w, *t_lid = p_lid, *t_dst = T.p_dst;
   if constexpr (LINKS_SMEM) {
     t_src = reinterpret_cast<const uint32_t *>(links_base + lay.off_tsrc);
     t_w = reinterpret_cast<const uint32_t *>(links_base + lay.off_tw);
     t_lid = reinterpret_cast<const uint32_t *>(links_base + lay.off_tlid);
+    t_dst = reinterpret_cast<const uint32_t *>(links_base + lay.off_tdst);
   }
   uint32_t *hver = reinterpret_cast<uint32_t *>(smem + lay.off_hver);
   uint32_t *bitmap2 = reinterpret_cast<uint32_t *>(smem + lay.off_bitmap);  // 2 x nbw words (event parity)
@@ -117,27 +120,35 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     if (Q > 1) cluster.sync();
     else __syncthreads();
   };
-  // source version of NPU x (owned by CTA x / chunkN)
+  // owner CTA of NPU x = x / chunkN, by a multiply-high with m = ceil(2^32 / chunkN):
+  // exact while x * (m * chunkN - 2^32) < 2^32, i.e. for N < 2^16
+  const uint32_t own_magic = (uint32_t)((0xFFFFFFFFull + chunkN) / chunkN);
+  auto owner_of = [&](uint32_t x) -> uint32_t { return N < 65536u ? __umulhi(x, own_magic) : x / chunkN; };
+  // source version of NPU x (owned by CTA owner_of(x))
   auto hver_of = [&](uint32_t x) -> uint32_t {
-    if (Q == 1 || x - d_lo < d_hi - d_lo) return hver[x];  // own NPU (the common case): no division
-    return dsmem_ld(dsmem_addr(hver + x, x / chunkN));
+    if (Q == 1 || x - d_lo < d_hi - d_lo) return hver[x];  // own NPU (the common case)
+    return dsmem_ld(dsmem_addr(hver + x, owner_of(x)));
   };
 
   // ---- a2: state init (P:L89 precondition; P:L212 start at t = 0) ----
   const uint32_t NW = N * Wp;
   for (uint32_t i = d_lo * Wp + tid; i < d_hi * Wp; i += nthr) {
-    uint32_t v;
+    uint32_t v, hv0;
     const uint32_t x = i / Wp, q = i - x * Wp;
     if (custom) {
+      // chunks d does not require are never candidates: have[d] starts as pre | ~post
+      // (with relays the per-link allow rows take that role)
       v = __ldg(&T.pre[i]);
+      hv0 = MASKED ? v : (v | ~__ldg(&T.post[i]));
     } else {  // AG: chunks x*k .. x*k+k-1 (R12)
       const uint32_t lo = x * T.k, hi = lo + T.k, wlo = q * 32u, whi = wlo + 32u;
       const uint32_t a = lo > wlo ? lo : wlo, b = hi < whi ? hi : whi;
       v = 0u;
       if (a < b) v = ((b - a) == 32u ? 0xFFFFFFFFu : ((1u << (b - a)) - 1u)) << (a - wlo);
+      hv0 = v;
     }
     held[(size_t)x * Wr + q] = v;
-    have[(size_t)x * Wr + q] = v;
+    have[(size_t)x * Wr + q] = hv0;
   }
   for (uint32_t p = p_lo + tid; p < p_hi; p += nthr) {
     busy[p] = 0ull;
@@ -147,6 +158,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       const_cast<uint32_t *>(t_src)[p] = __ldg(&p_src[p]);
       const_cast<uint32_t *>(t_w)[p] = __ldg(&p_w[p]);
       const_cast<uint32_t *>(t_lid)[p] = __ldg(&p_lid[p]);
+      const_cast<uint32_t *>(t_dst)[p] = __ldg(&T.p_dst[p]);
     }
   }
   for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) hver[x] = 0u;
@@ -173,8 +185,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t gmask = (P == 32) ? 0xFFFFFFFFu : (((1u << P) - 1u) << (lane & ~(uint32_t)(P - 1)));
   const uint32_t ngroups = nthr / P;
   const bool pre_draw = lay.pre_draw != 0u;
-  // PA: threads [0, nA) handle destinations; with pre_draw the others draw Philox values
-  const uint32_t nA = pre_draw ? max(32u, min(nthr / 2u, ((d_hi - d_lo) + 31u) & ~31u)) : nthr;
   const bool tracing = job.trace != nullptr && tid == 0;
 
   for (;;) {
@@ -185,59 +195,52 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       const uint32_t rec_base = s_rec_base;
       const uint32_t *bm_prev = bitmap2 + ((e + 1u) & 1u) * nbw;  // bitmap of event e-1
       uint32_t arr = 0;
-      // one thread per destination: its in-links are contiguous positions, so the
-      // held row is updated without atomics.  With pre_draw, threads [nA, nthr)
-      // draw the Philox values of every link free at t meanwhile (t and busy_until
-      // are fixed here; liveness is decided in PM after the arrivals).
-      if (tid >= nA) {
-        constexpr int kPB = 4;  // positions per pass: branch-free Philox chains interleave (ILP)
-        const uint32_t nD = nthr - nA;
-        for (uint32_t base = p_lo + (tid - nA); base < p_hi; base += nD * kPB) {
-          uint32_t lidv[kPB];
+      // one thread per in-link position (kPB positions per pass, interleaved for ILP):
+      // the record of the previous event, the arrival (a shared-memory atomicOr on the
+      // destination's held row) and, with pre_draw, the Philox draws of every link free
+      // at t (t and busy_until are fixed here; liveness is decided in PM after the arrivals).
+      constexpr int kPB = 4;
+      for (uint32_t base = p_lo + tid; base < p_hi; base += nthr * kPB) {
+        uint4 r[kPB];
+        if (pre_draw) {
 #pragma unroll
           for (int u = 0; u < kPB; ++u) {
-            const uint32_t q = base + (uint32_t)u * nD;
-            lidv[u] = q < p_hi ? t_lid[q] : 0u;
+            const uint32_t q = base + (uint32_t)u * nthr;
+            r[u] = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), q < p_hi ? t_lid[q] : 0u, job.sigma),
+                                 seed_lo, seed_hi);
           }
-          uint4 r[kPB];
+        }
 #pragma unroll
-          for (int u = 0; u < kPB; ++u)
-            r[u] = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), lidv[u], job.sigma), seed_lo, seed_hi);
-#pragma unroll
-          for (int u = 0; u < kPB; ++u) {
-            const uint32_t q = base + (uint32_t)u * nD;
-            if (q < p_hi && busy[q] <= t) {
-              ord[q] = r[u].x;
-              pick[q] = r[u].y;
+        for (int u = 0; u < kPB; ++u) {
+          const uint32_t q = base + (uint32_t)u * nthr;
+          if (q >= p_hi) break;
+          const unsigned long long b = busy[q];
+          const uint32_t c = cur[q];
+          if (c != kNone) {
+            if (rec != nullptr && e > 0u && b - t_w[q] == t_prev) {
+              const uint32_t lid = t_lid[q];
+              const uint32_t wi = lid >> 5;
+              const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
+              Rec rc;
+              rc.chunk = c;
+              rc.link = lid;
+              rc.t_start = t_prev;
+              rec[idx] = rc;
+            }
+            if (b == t) {  // R7: held by dst from this instant
+              const uint32_t d = t_dst[q];
+              atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
+              hver[d] = e;
+              cur[q] = kNone;
+              // a relayed chunk (not in post[d]) is held but not required
+              if (!MASKED || ((__ldg(&T.post[(size_t)d * Wp + (c >> 5)]) >> (c & 31u)) & 1u)) ++arr;
             }
           }
-        }
-      }
-      for (uint32_t d = d_lo + tid; d < d_hi && tid < nA; d += nA) {
-        const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
-        bool got = false;
-        for (uint32_t p = b0; p < b1; ++p) {
-          const uint32_t c = cur[p];
-          if (c == kNone) continue;
-          const unsigned long long b = busy[p];
-          if (rec != nullptr && e > 0u && b - t_w[p] == t_prev) {
-            const uint32_t lid = t_lid[p];
-            const uint32_t wi = lid >> 5;
-            const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
-            Rec r;
-            r.chunk = c;
-            r.link = lid;
-            r.t_start = t_prev;
-            rec[idx] = r;
-          }
-          if (b == t) {  // R7: held by dst from this instant
-            held[(size_t)d * Wr + (c >> 5)] |= 1u << (c & 31u);
-            cur[p] = kNone;
-            got = true;
-            ++arr;
+          if (pre_draw && b <= t) {
+            ord[q] = r[u].x;
+            pick[q] = r[u].y;
           }
         }
-        if (got) hver[d] = e;
       }
       arr = warp_sum_u32(arr);
       if (lane == 0 && arr) atomicAdd(&s_delivered, (unsigned long long)arr);  // own deliveries, cumulative
@@ -311,7 +314,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         const uint32_t deg = b1 - b0;
         uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
-        const uint4 *post4 = reinterpret_cast<const uint4 *>(T.post + (size_t)d * Wp);
         uint4 hv[V];
 
         // One step of the matching walk (a5) on in-link position p with pick draw pk.
@@ -329,7 +331,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
           } else {  // source row in a peer CTA's shared memory (DSMEM)
-            const uint32_t a = dsmem_addr(held + (size_t)sp * Wr, sp / chunkN);
+            const uint32_t a = dsmem_addr(held + (size_t)sp * Wr, owner_of(sp));
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(v * P + gl) * 16u);
           }
@@ -342,7 +344,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (int v = 0; v < V; ++v) {
             if constexpr (kHaveSmem) cv[v] = andnot4(cv[v], have4[v * P + gl]);  // held[src] & ~have[d]
             else cv[v] = andnot4(cv[v], hv[v]);
-            if (custom) cv[v] = and4(cv[v], __ldg(&post4[v * P + gl]));  // & post[d]
+            if constexpr (MASKED)  // & allow[p]: post[d] plus the relays of this link
+              cv[v] = and4(cv[v], __ldg(reinterpret_cast<const uint4 *>(T.allow + (size_t)p * Wp) + v * P + gl));
             incl[v] = popc4(cv[v]);
 #pragma unroll
             for (int o = 1; o < P; o <<= 1) {
@@ -419,7 +422,77 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         };
 
         // REG_PATH (every in-degree <= kRegDeg): ranks in registers; else shared memory
-        if constexpr (REG_PATH) {
+        if constexpr (REG_PATH && P == 1) {
+          // ---- one thread per destination: in-link j in slot j (static), ranks by the
+          //      28 pairwise comparisons, walk order packed 4 bits per rank, and the
+          //      next in-link's source row loaded while the current one is matched ----
+          unsigned long long key[kRegDeg];
+          uint32_t nfree = 0, nlive = 0;
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) {
+            key[j] = ~0ull;
+            if ((uint32_t)j < deg) {
+              const uint32_t q = b0 + (uint32_t)j;
+              const bool isfree = busy[q] <= t;
+              const bool islive = isfree && seen[q] != hver_of(t_src[q]);
+              nfree += isfree ? 1u : 0u;
+              if (islive) {
+                uint32_t o;
+                if (pre_draw) {
+                  o = ord[q];
+                } else {
+                  const uint4 r = philox4x32_10(
+                      make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
+                  o = r.x;
+                  pick[q] = r.y;
+                }
+                ++nlive;
+                key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
+              }
+            }
+          }
+          if (!worklist) {
+            myV += nfree;
+            myD += nfree ? 1u : 0u;
+          }
+          if (nlive == 0u) continue;
+          // rank of slot j = #{i : key_i < key_j or (key_i == key_j and i < j)}; non-live keys
+          // (~0, above every live key: w < 2^32 - 1 is enforced on the host) rank last
+          uint32_t rk[kRegDeg];
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) rk[j] = 0u;
+#pragma unroll
+          for (int i = 0; i < kRegDeg; ++i)
+#pragma unroll
+            for (int j = i + 1; j < kRegDeg; ++j) {
+              const bool jfirst = key[j] < key[i];
+              rk[i] += jfirst ? 1u : 0u;
+              rk[j] += jfirst ? 0u : 1u;
+            }
+          uint32_t ordp = 0;  // slot of rank s in bits [4s, 4s + 4)
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
+          uint4 nxt[V];
+          load_row(b0 + (ordp & 15u), nxt);
+          for (uint32_t s = 0; s < nlive; ++s) {
+            const uint32_t p = b0 + ((ordp >> (4u * s)) & 15u);
+            uint4 cv[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) cv[v] = nxt[v];
+            if (s + 1u < nlive) load_row(b0 + ((ordp >> (4u * s + 4u)) & 15u), nxt);
+            if constexpr (!kHaveSmem) {
+              if (s == 0u) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) hv[v] = have4[v];
+              }
+            }
+            step_row(p, pick[p], cv);
+          }
+          if constexpr (!kHaveSmem) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) have4[v] = hv[v];
+          }
+        } else if constexpr (REG_PATH) {
           // ---- register path: the group owns the destination's <= kRegDeg in-links, in-link j
           //      in slot j / P of lane j % P; ranks and the walk order stay in registers ----
           constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
@@ -694,9 +767,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   }
 }
 
-template <int P, int V, bool R, bool K, bool G>
+template <int P, int V, bool R, bool K, bool G, bool M = false>
 int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
-  auto fn = greedy_kernel<P, V, R, K, G>;
+  auto fn = greedy_kernel<P, V, R, K, G, M>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.smem_bytes);
   if (e != cudaSuccess) {
     snprintf(cuda_error_buffer(), 256, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -730,6 +803,11 @@ int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, Job
 
 template <int P, int V>
 int launch_greedy_pv(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
+  if (lay.masked) {  // relays: shared-memory ranking path only
+    if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true, false, true>(lay, d_jobs, n_jobs, d_outs, st);
+    if (lay.links_in_smem) return launch_greedy_one<P, V, false, true, false, true>(lay, d_jobs, n_jobs, d_outs, st);
+    return launch_greedy_one<P, V, false, false, false, true>(lay, d_jobs, n_jobs, d_outs, st);
+  }
   if (lay.reg_path) {
     if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true, true>(lay, d_jobs, n_jobs, d_outs, st);
     if (lay.links_in_smem) return launch_greedy_one<P, V, false, true, true>(lay, d_jobs, n_jobs, d_outs, st);

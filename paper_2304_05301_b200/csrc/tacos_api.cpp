@@ -343,6 +343,7 @@ struct Part {
   uint32_t N = 0, L = 0, C = 0, k = 0, Wp = 0, P = 0, VPL = 0;
   bool custom = false, symmetric = false, rs_search = false;
   uint64_t required = 0;
+  uint64_t cap = 0;  // send records per job (= required without relays)
   std::vector<uint32_t> w;
   DevTopo htopo[2];
   DevTopo *d_topo[2] = {nullptr, nullptr};
@@ -377,6 +378,7 @@ struct tacos_plan {
   std::vector<DevBuf> bufs;
   uint32_t last_launches = 0;
   unsigned long long *d_trace = nullptr;
+  unsigned long long *d_count = nullptr;  // compact_sends result (relays)
   ~tacos_plan() {
     for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
     if (h_small_buf.p) pinned_pool().release(h_small_buf.dev, h_small_buf.p, h_small_buf.cls);
@@ -384,10 +386,111 @@ struct tacos_plan {
 };
 
 namespace {
+// collective classes (tacos.h): named = rooted collectives of row f2
+bool coll_named(int c) { return c >= TACOS_BROADCAST && c <= TACOS_GATHER; }
+bool coll_custom(int c) { return c == TACOS_CUSTOM || coll_named(c); }
+bool coll_need_rs(int c) {
+  return c == TACOS_REDUCE_SCATTER || c == TACOS_ALL_REDUCE || c == TACOS_REDUCE || c == TACOS_GATHER;
+}
+bool coll_need_ag(int c) { return !(c == TACOS_REDUCE_SCATTER || c == TACOS_REDUCE || c == TACOS_GATHER); }
+bool coll_relay(const tacos_synth_params *p) {
+  return (p->flags & TACOS_FLAG_RELAY) != 0u || p->collective == TACOS_SCATTER || p->collective == TACOS_GATHER;
+}
+
+// Pre/post rows (W0 = ceil(C/32) words per NPU) of the searched forward problem
+// (§II.A; P:L70 Fig. CollectiveDefinition): the caller's for CUSTOM; for
+// BROADCAST / REDUCE the Broadcast from root, for SCATTER / GATHER the Scatter
+// from root (REDUCE and GATHER are its inverse on G^T).
+int problem_bits(uint32_t N, const tacos_synth_params *p, uint32_t &C, std::vector<uint32_t> &pre,
+                 std::vector<uint32_t> &post) {
+  const int c = p->collective;
+  if (c == TACOS_CUSTOM) {
+    C = p->n_chunks;
+    const uint32_t W0 = (C + 31u) / 32u;
+    pre.assign(p->pre_bits, p->pre_bits + (size_t)N * W0);
+    post.assign(p->post_bits, p->post_bits + (size_t)N * W0);
+    return TACOS_OK;
+  }
+  const uint32_t k = p->chunks_per_npu, root = p->root;
+  if (root >= N) return fail(TACOS_E_INVALID_ARG, "root %u out of range", root);
+  const bool bcast = c == TACOS_BROADCAST || c == TACOS_REDUCE;
+  const uint64_t C64 = bcast ? (uint64_t)k : (uint64_t)N * k;
+  if (C64 > kMaxChunks) return fail(TACOS_E_OVERFLOW, "C = %llu chunks exceeds %u", (unsigned long long)C64, kMaxChunks);
+  C = (uint32_t)C64;
+  const uint32_t W0 = (C + 31u) / 32u;
+  pre.assign((size_t)N * W0, 0u);
+  post.assign((size_t)N * W0, 0u);
+  auto set = [&](std::vector<uint32_t> &v, uint32_t x, uint32_t ch) { v[(size_t)x * W0 + (ch >> 5)] |= 1u << (ch & 31u); };
+  for (uint32_t ch = 0; ch < C; ++ch) {
+    set(pre, root, ch);
+    set(post, root, ch);
+    if (bcast)
+      for (uint32_t x = 0; x < N; ++x) set(post, x, ch);
+    else
+      set(post, ch / k, ch);  // Scatter: NPU x requires chunks x*k .. x*k+k-1
+  }
+  return TACOS_OK;
+}
+
+// R22 relay masks in the position order of orientation o (0: links as given,
+// 1: reversed): allow[q] = post[d] plus the chunks c that d may relay, i.e. d does
+// not require c and is one hop closer than s to the nearest NPU that requires c
+// and lacks it at the start (hop BFS over the oriented links).  Wp words per row.
+void relay_allow(const tacos_topology *t, int o, uint32_t C, uint32_t Wp, const std::vector<uint32_t> &pre,
+                 const std::vector<uint32_t> &post, std::vector<uint32_t> &allow) {
+  const uint32_t N = (uint32_t)t->N, L = (uint32_t)t->L, W0 = (C + 31u) / 32u;
+  const auto &ptr = t->in_ptr[o];
+  const auto &ps = t->pos_src[o];
+  const auto &pd = t->pos_dst[o];
+  auto bit = [&](const std::vector<uint32_t> &v, uint32_t x, uint32_t ch) {
+    return ((v[(size_t)x * W0 + (ch >> 5)] >> (ch & 31u)) & 1u) != 0u;
+  };
+  allow.assign((size_t)L * Wp, 0u);
+  for (uint32_t q = 0; q < L; ++q)
+    for (uint32_t i = 0; i < W0; ++i) allow[(size_t)q * Wp + i] = post[(size_t)pd[q] * W0 + i];
+  std::vector<uint32_t> req, prev_req;
+  std::vector<int32_t> dist(N, -1);
+  std::vector<uint32_t> queue;
+  for (uint32_t ch = 0; ch < C; ++ch) {
+    req.clear();
+    for (uint32_t x = 0; x < N; ++x)
+      if (bit(post, x, ch) && !bit(pre, x, ch)) req.push_back(x);
+    if (req.empty()) continue;
+    if (req != prev_req) {  // multi-source BFS backwards along in-links
+      std::fill(dist.begin(), dist.end(), -1);
+      queue.clear();
+      for (uint32_t x : req) {
+        dist[x] = 0;
+        queue.push_back(x);
+      }
+      for (size_t h = 0; h < queue.size(); ++h) {
+        const uint32_t y = queue[h];
+        for (uint32_t q = ptr[y]; q < ptr[y + 1]; ++q) {
+          const uint32_t x = ps[q];
+          if (dist[x] < 0) {
+            dist[x] = dist[y] + 1;
+            queue.push_back(x);
+          }
+        }
+      }
+      prev_req = req;
+    }
+    for (uint32_t q = 0; q < L; ++q) {
+      const uint32_t s = ps[q], d = pd[q];
+      if (!bit(post, d, ch) && dist[d] >= 0 && dist[s] == dist[d] + 1)
+        allow[(size_t)q * Wp + (ch >> 5)] |= 1u << (ch & 31u);
+    }
+  }
+}
+
 int validate_params(const tacos_synth_params *p) {
   if (!p) return fail(TACOS_E_INVALID_ARG, "null params");
-  if (p->collective < TACOS_ALL_GATHER || p->collective > TACOS_CUSTOM)
+  if (p->collective < TACOS_ALL_GATHER || p->collective > TACOS_GATHER)
     return fail(TACOS_E_INVALID_ARG, "bad collective %d", p->collective);
+  if (coll_relay(p) && !coll_custom(p->collective))
+    return fail(TACOS_E_INVALID_ARG, "relays apply to CUSTOM and rooted collectives");
+  if (coll_relay(p) && (p->flags & TACOS_FLAG_LITERAL))
+    return fail(TACOS_E_INVALID_ARG, "relays are not supported by the paper-literal variant");
   if (p->chunk_bytes == 0) return fail(TACOS_E_INVALID_ARG, "chunk_bytes = 0");
   if (p->n_seeds < 1) return fail(TACOS_E_INVALID_ARG, "n_seeds = 0");
   if ((uint64_t)p->seed_offset + p->n_seeds > (1ull << kKeySeedBits))
@@ -418,8 +521,9 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   pl->p = *p;
   if (pl->p.time_unit_ns == 0) pl->p.time_unit_ns = 1;
   const uint32_t S = p->n_seeds;
-  const bool custom = p->collective == TACOS_CUSTOM;
-  const bool need_rs = p->collective == TACOS_REDUCE_SCATTER || p->collective == TACOS_ALL_REDUCE;
+  const bool custom = coll_custom(p->collective);
+  const bool need_rs = coll_need_rs(p->collective);
+  const bool relay = coll_relay(p);
   const bool record = (p->flags & TACOS_FLAG_NO_SCHEDULE) == 0;
 
   // ---- per-topology host preparation ----
@@ -435,7 +539,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     pt.L = (uint32_t)t->L;
     pt.custom = custom;
     if (custom) {
-      pt.C = p->n_chunks;
+      if (n_topos != 1) return fail(TACOS_E_INVALID_ARG, "CUSTOM and rooted collectives are not batched over topologies");
+      if ((rc = problem_bits(pt.N, p, pt.C, pl->pre, pl->post))) return rc;
       pt.k = 0;
     } else {
       const uint64_t C = (uint64_t)pt.N * p->chunks_per_npu;
@@ -464,20 +569,21 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     if (pt.VPL > (uint32_t)kMaxVPL) return fail(TACOS_E_OVERFLOW, "C too large");
     pt.Wp = 4u * pt.P * pt.VPL;
     if (custom) {
-      if (n_topos != 1) return fail(TACOS_E_INVALID_ARG, "CUSTOM collectives are not batched over topologies");
       const size_t words = (size_t)pt.N * W0;
-      pl->pre.assign(p->pre_bits, p->pre_bits + words);
-      pl->post.assign(p->post_bits, p->post_bits + words);
-      uint64_t req = 0;
+      uint64_t req = 0, held0 = 0;
       for (size_t q = 0; q < words; ++q) {
         if (pl->pre[q] & ~pl->post[q]) return fail(TACOS_E_INVALID_ARG, "pre is not a subset of post (row %zu)", q / W0);
         const uint32_t valid = (q % W0 == W0 - 1 && (pt.C & 31u)) ? ((1u << (pt.C & 31u)) - 1u) : 0xFFFFFFFFu;
         if ((pl->pre[q] | pl->post[q]) & ~valid) return fail(TACOS_E_INVALID_ARG, "bits beyond C set");
         req += (uint64_t)__builtin_popcount(pl->post[q] & ~pl->pre[q]);
+        held0 += (uint64_t)__builtin_popcount(pl->pre[q]);
       }
       pt.required = req;
+      // records per job: every (NPU, chunk) pair is delivered at most once (relays add sends)
+      pt.cap = relay ? (uint64_t)pt.N * pt.C - held0 : req;
     } else {
       pt.required = (uint64_t)pt.C * (pt.N - 1u);
+      pt.cap = pt.required;
     }
     pt.job_base = n_jobs;
     pt.n_jobs = S * (pt.rs_search ? 2u : 1u);
@@ -528,6 +634,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       g.lay.cluster = 1;
     }
     if (const char *env = getenv("TACOS_REG_PATH")) g.lay.reg_path = (uint32_t)atoi(env);
+    g.lay.masked = relay ? 1u : 0u;
+    if (relay) g.lay.reg_path = 0u;  // the masked kernels are instantiated on the shared-memory ranking path
     // worklist for sparse events: several distinct link costs free only some links per event
     bool multi_w = false;
     for (size_t gk = gi; gk < gj && !multi_w; ++gk) {
@@ -565,6 +673,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   }
   if ((rc = dev_alloc(bufs, dev, sizeof(JobOut) * n_jobs, &vp))) return rc;
   pl->d_outs = reinterpret_cast<JobOut *>(vp);
+  if ((rc = dev_alloc(bufs, dev, 8, &vp))) return rc;
+  pl->d_count = reinterpret_cast<unsigned long long *>(vp);
   uint64_t max_M = 0;
   for (uint32_t i = 0; i < n_topos; ++i) {
     Part &pt = pl->parts[i];
@@ -577,7 +687,14 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       for (uint32_t q = 0; q < pt.L; ++q) pw[q] = pt.w[t->pos_lid[o][q]];
       if ((rc = upload(bufs, dev, pw.data(), pw.size(), &d_pos_w[o]))) return rc;
     }
-    uint32_t *d_pre = nullptr, *d_post = nullptr;
+    uint32_t *d_pre = nullptr, *d_post = nullptr, *d_allow[2] = {nullptr, nullptr};
+    if (relay) {
+      for (int o = 0; o < 2; ++o) {
+        std::vector<uint32_t> allow;
+        relay_allow(t, o, pt.C, pt.Wp, pl->pre, pl->post, allow);
+        if ((rc = upload(bufs, dev, allow.data(), allow.size(), &d_allow[o]))) return rc;
+      }
+    }
     if (custom) {
       const uint32_t W0 = (pt.C + 31u) / 32u;
       std::vector<uint32_t> pre_p((size_t)pt.N * pt.Wp, 0u), post_p((size_t)pt.N * pt.Wp, 0u);
@@ -607,10 +724,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       h.p_lid = t->d_pos_lid[o];
       h.pre = d_pre;
       h.post = d_post;
+      h.allow = d_allow[o];
       if ((rc = upload(bufs, dev, &h, 1, &pt.d_topo[o]))) return rc;
     }
     if (record) {
-      if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.required * pt.n_jobs, &vp))) return rc;
+      if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.cap * pt.n_jobs, &vp))) return rc;
       pt.d_rec = reinterpret_cast<Rec *>(vp);
     }
     if ((rc = dev_alloc(bufs, dev, 8 * 8, &vp))) return rc;
@@ -622,7 +740,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       if ((rc = dev_alloc(bufs, dev, 8 * (size_t)S, &vp))) return rc;
       pt.d_times_rs = reinterpret_cast<uint64_t *>(vp);
     }
-    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL)) && record) max_M = std::max(max_M, pt.required);
+    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL)) && record) max_M = std::max(max_M, pt.cap);
   }
   if (max_M) {
     pl->sort_bytes = rs_sort_scratch_bytes(max_M);
@@ -643,7 +761,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         jb.seed = p->base_seed + p->seed_offset + si;
         jb.sigma = sigma;
         jb.out_slot = pt.job_base + j;
-        jb.rec = record ? pt.d_rec + (size_t)j * pt.required : nullptr;
+        jb.rec = record ? pt.d_rec + (size_t)j * pt.cap : nullptr;
         jb.g_rows = nullptr;
         jb.g_links = nullptr;
         jb.trace = nullptr;
@@ -702,9 +820,10 @@ int plan_read_small(tacos_plan *pl, cudaStream_t st) {
   return TACOS_OK;
 }
 
+// upper bound of the sends of one result (exact without relays)
 uint64_t sends_per_result(const tacos_plan *pl, const Part &pt) {
   if (pl->p.flags & TACOS_FLAG_NO_SCHEDULE) return 0;
-  return pl->p.collective == TACOS_ALL_REDUCE ? 2 * pt.required : pt.required;
+  return pl->p.collective == TACOS_ALL_REDUCE ? 2 * pt.cap : pt.cap;
 }
 
 // Emit part i's schedule into device memory d_sends; fill res from the keys in h_small.
@@ -724,8 +843,8 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   res->best_key_rs = key_rs;
   const int32_t st_status = (int32_t)(int64_t)stats[4];
   const int coll = pl->p.collective;
-  const bool need_rs = coll == TACOS_REDUCE_SCATTER || coll == TACOS_ALL_REDUCE;
-  const bool need_ag = coll != TACOS_REDUCE_SCATTER;
+  const bool need_rs = coll_need_rs(coll);
+  const bool need_ag = coll_need_ag(coll);
   tacos_winner win;
   const uint64_t keys[2] = {key_ag, key_rs};
   int rc0 = tacos_select_winner(keys, coll, pt.symmetric ? 1 : 0, pl->p.seed_offset, pl->p.n_seeds, &win);
@@ -748,23 +867,52 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   const uint64_t nsend = sends_per_result(pl, pt);
   if (nsend == 0) return TACOS_OK;
   if (capacity < nsend) return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)capacity, (unsigned long long)nsend);
-  const uint64_t M = pt.required;
   const tacos_topology *t = pt.topo;
   int rc;
   uint64_t emitted = 0;
+  // matches of a winning job: `required` without relays, else read back from its JobOut
+  auto job_matches = [&](uint32_t job, uint64_t *m) -> int {
+    if (!coll_relay(&pl->p)) {
+      *m = pt.required;
+      return TACOS_OK;
+    }
+    JobOut o;
+    CUDA_TRY(cudaMemcpyAsync(&o, pl->d_outs + pt.job_base + job, sizeof(o), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *m = o.M;
+    return TACOS_OK;
+  };
+  // relays (R22): drop the sends still in flight when the postcondition held (tombstones
+  // written by the emitters), order preserved; *m = the sends kept
+  auto drop_late = [&](tacos_send *first, uint64_t *m) -> int {
+    if (!coll_relay(&pl->p) || *m == 0) return TACOS_OK;
+    int r = launch_compact_sends(first, *m, pl->d_count, st);
+    if (r) return fail(r, "%s", cuda_error_string());
+    pl->last_launches += 1;
+    unsigned long long kept = 0;
+    CUDA_TRY(cudaMemcpyAsync(&kept, pl->d_count, sizeof(kept), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    *m = kept;
+    return TACOS_OK;
+  };
   if (need_rs && rs_local) {
     const uint32_t job = pt.symmetric ? (uint32_t)(g_rs - off) : S + (uint32_t)(g_rs - off);
-    const Rec *rec = pt.d_rec + (size_t)job * M;
+    uint64_t M;
+    if ((rc = job_matches(job, &M))) return rc;
+    const Rec *rec = pt.d_rec + (size_t)job * pt.cap;
     uint32_t nl = 0;
     if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, pt.symmetric ? t->d_rev : nullptr, T_rs, pt.L,
                                   d_sends, pl->d_sort, pl->sort_bytes, &nl, st)))
       return fail(rc, "%s", cuda_error_string());
     pl->last_launches += nl;
+    if ((rc = drop_late(d_sends, &M))) return rc;
     emitted += M;
   }
   if (need_ag && ag_local) {
-    const Rec *rec = pt.d_rec + (size_t)(g_ag - off) * M;
-    const uint64_t base = coll == TACOS_ALL_REDUCE ? M : 0;
+    uint64_t M;
+    if ((rc = job_matches((uint32_t)(g_ag - off), &M))) return rc;
+    const Rec *rec = pt.d_rec + (size_t)(g_ag - off) * pt.cap;
+    const uint64_t base = coll == TACOS_ALL_REDUCE ? pt.required : 0;  // AR: after the RS half (no relays)
     if (pl->p.flags & TACOS_FLAG_LITERAL) {  // records in delivery order: sort by (t_start, link)
       uint32_t nl = 0;
       if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, nullptr, T_ag, pt.L, d_sends + base, pl->d_sort,
@@ -772,10 +920,11 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
         return fail(rc, "%s", cuda_error_string());
       pl->last_launches += nl;
     } else {
-      if ((rc = launch_emit_ag(rec, M, t->d_src, t->d_dst, pt.d_w, T_rs, d_sends + base, st)))
+      if ((rc = launch_emit_ag(rec, M, t->d_src, t->d_dst, pt.d_w, T_rs, d_sends + base, st, T_rs + T_ag)))
         return fail(rc, "%s", cuda_error_string());
       pl->last_launches += 1;
     }
+    if ((rc = drop_late(d_sends + base, &M))) return rc;
     emitted += M;
   }
   res->n_sends = emitted;
@@ -786,10 +935,10 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
 extern "C" int tacos_select_winner(const uint64_t keys[2], int32_t collective, int symmetric, uint32_t seed_offset,
                                    uint32_t n_seeds, tacos_winner *out) {
   if (!keys || !out) return fail(TACOS_E_INVALID_ARG, "null argument");
-  if (collective < TACOS_ALL_GATHER || collective > TACOS_CUSTOM) return fail(TACOS_E_INVALID_ARG, "bad collective");
+  if (collective < TACOS_ALL_GATHER || collective > TACOS_GATHER) return fail(TACOS_E_INVALID_ARG, "bad collective");
   std::memset(out, 0, sizeof(*out));
-  const bool need_rs = collective == TACOS_REDUCE_SCATTER || collective == TACOS_ALL_REDUCE;
-  const bool need_ag = collective != TACOS_REDUCE_SCATTER;
+  const bool need_rs = coll_need_rs(collective);
+  const bool need_ag = coll_need_ag(collective);
   // the RS phase of a symmetric graph is the mirror of the AG winner (R9); else its own search (key 1)
   const bool rs_own = need_rs && !symmetric;
   const uint64_t k_ag = keys[0], k_rs = rs_own ? keys[1] : keys[0];
@@ -881,10 +1030,21 @@ extern "C" int tacos_max_sends(const tacos_topology *topo, const tacos_synth_par
   int rc = validate_params(p);
   if (rc) return rc;
   uint64_t M;
-  if (p->collective == TACOS_CUSTOM) {
-    const uint32_t W0 = (p->n_chunks + 31u) / 32u;
+  if (coll_custom(p->collective)) {
+    uint32_t C = 0;
+    std::vector<uint32_t> pre, post;
+    try {
+      if ((rc = problem_bits((uint32_t)topo->N, p, C, pre, post))) return rc;
+    } catch (const std::bad_alloc &) {
+      return fail(TACOS_E_NOMEM, "host allocation failed");
+    }
     M = 0;
-    for (size_t q = 0; q < (size_t)topo->N * W0; ++q) M += (uint64_t)__builtin_popcount(p->post_bits[q] & ~p->pre_bits[q]);
+    uint64_t held0 = 0;
+    for (size_t q = 0; q < pre.size(); ++q) {
+      M += (uint64_t)__builtin_popcount(post[q] & ~pre[q]);
+      held0 += (uint64_t)__builtin_popcount(pre[q]);
+    }
+    if (coll_relay(p)) M = (uint64_t)topo->N * C - held0;  // upper bound: each (NPU, chunk) delivered at most once
   } else {
     M = (uint64_t)topo->N * p->chunks_per_npu * (uint64_t)(topo->N - 1);
   }
@@ -942,8 +1102,8 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       d_out = reinterpret_cast<tacos_send *>(tmp.p);
     }
     rc = plan_emit_part(pl.get(), i, d_out, need, &results[i], st);
-    if (rc == TACOS_OK && need > 0 && !dev_out) {
-      cudaError_t e = cudaMemcpyAsync(dst[i], d_out, need * sizeof(tacos_send), cudaMemcpyDeviceToHost, st);
+    if (rc == TACOS_OK && results[i].n_sends > 0 && !dev_out) {
+      cudaError_t e = cudaMemcpyAsync(dst[i], d_out, results[i].n_sends * sizeof(tacos_send), cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "D2H of the schedule: %s", cudaGetErrorString(e));
     }
     if (rc == TACOS_OK && seed_times) {
@@ -1125,11 +1285,9 @@ extern "C" int tacos_eval(const tacos_topology *t, const tacos_synth_params *p, 
     uint32_t C;
     std::vector<uint32_t> pre, post;
     uint32_t W0;
-    if (p->collective == TACOS_CUSTOM) {
-      C = p->n_chunks;
+    if (coll_custom(p->collective)) {  // REDUCE / GATHER: the forward problem, checked on G^T below
+      if ((rc = problem_bits(N, p, C, pre, post))) return rc;
       W0 = (C + 31) / 32;
-      pre.assign(p->pre_bits, p->pre_bits + (size_t)N * W0);
-      post.assign(p->post_bits, p->post_bits + (size_t)N * W0);
     } else {
       C = N * p->chunks_per_npu;
       W0 = (C + 31) / 32;
@@ -1148,7 +1306,7 @@ extern "C" int tacos_eval(const tacos_topology *t, const tacos_synth_params *p, 
     std::vector<tacos_send> all(sends, sends + n_sends);
     std::vector<uint64_t> idx(n_sends);
     for (uint64_t i = 0; i < n_sends; ++i) idx[i] = i;
-    if (p->collective == TACOS_ALL_GATHER || p->collective == TACOS_CUSTOM) {
+    if (!coll_need_rs(p->collective)) {  // AG, CUSTOM, BROADCAST, SCATTER
       check_phase(t, w, 0, all, idx, C, pre, post, W0, ck);
       return TACOS_OK;
     }
@@ -1394,10 +1552,11 @@ namespace {
 int params_chunks(const tacos_topology *t, const tacos_synth_params *p, uint32_t &C, std::vector<uint32_t> &pre,
                   uint32_t &W0) {
   const uint32_t N = (uint32_t)t->N;
-  if (p->collective == TACOS_CUSTOM) {
-    C = p->n_chunks;
+  if (coll_custom(p->collective)) {
+    std::vector<uint32_t> post;
+    int rc = problem_bits(N, p, C, pre, post);
+    if (rc) return rc;
     W0 = (C + 31) / 32;
-    pre.assign(p->pre_bits, p->pre_bits + (size_t)N * W0);
   } else {
     C = N * p->chunks_per_npu;
     W0 = (C + 31) / 32;
@@ -1423,7 +1582,7 @@ extern "C" int tacos_eval_continuous(const tacos_topology *t, const tacos_synth_
     for (uint32_t l = 0; l < L; ++l) dur[l] = (double)t->alpha[l] + (double)p->chunk_bytes / (double)t->bw[l];
     uint32_t C, W0;
     std::vector<uint32_t> pre;
-    params_chunks(t, p, C, pre, W0);
+    if ((rc = params_chunks(t, p, C, pre, W0))) return rc;
     std::vector<uint64_t> ord(n_sends);
     for (uint64_t i = 0; i < n_sends; ++i) {
       const tacos_send &s = sends[i];
@@ -1432,7 +1591,9 @@ extern "C" int tacos_eval_continuous(const tacos_topology *t, const tacos_synth_
       ord[i] = i;
     }
     std::stable_sort(ord.begin(), ord.end(), [&](uint64_t a, uint64_t b) { return sends[a].t_start < sends[b].t_start; });
-    const bool ar = p->collective == TACOS_ALL_REDUCE, rs = p->collective == TACOS_REDUCE_SCATTER;
+    // reduction-phase replay for RS / REDUCE / GATHER (a node sends a chunk once everything it
+    // receives of that chunk has arrived; GATHER receives each chunk at most once)
+    const bool ar = p->collective == TACOS_ALL_REDUCE, rs = coll_need_rs(p->collective) && !ar;
     uint64_t n_rs = ar ? n_sends / 2 : (rs ? n_sends : 0);
     if (ar) {  // phase split by (t_start, link), as tacos_eval
       std::vector<uint64_t> o2(ord);
@@ -1589,7 +1750,7 @@ extern "C" int tacos_baseline(const tacos_topology *t, const tacos_synth_params 
   if (!t || !p || !n_out) return fail(TACOS_E_INVALID_ARG, "null argument");
   int rc = validate_params(p);
   if (rc) return rc;
-  if (p->collective == TACOS_CUSTOM) return fail(TACOS_E_INVALID_ARG, "baselines are defined for AG / RS / AR");
+  if (coll_custom(p->collective)) return fail(TACOS_E_INVALID_ARG, "baselines are defined for AG / RS / AR");
   if (algorithm != TACOS_BASELINE_RING && algorithm != TACOS_BASELINE_DIRECT)
     return fail(TACOS_E_INVALID_ARG, "unknown baseline %d", algorithm);
   try {

@@ -31,6 +31,7 @@ struct DevTopo {
   const uint32_t *p_lid;  // [L] link id (input index)
   const uint32_t *pre;    // [N*Wp] custom only
   const uint32_t *post;   // [N*Wp] custom only
+  const uint32_t *allow;  // [L*Wp] relays only (R22): chunks position p may carry, else nullptr
 };
 
 // Compact send record written by the search (16 B): ordered by (t_start, link)
@@ -67,7 +68,7 @@ struct Layout {
   uint32_t links_bytes;  // per-position arrays
   // within the links region
   uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv;
-  uint32_t off_tsrc, off_tw, off_tlid;  // per-position topology copies (src, w, link id)
+  uint32_t off_tsrc, off_tw, off_tlid, off_tdst;  // per-position topology copies (src, w, link id, dst)
   // always in shared memory, after [rows][links] when those are resident
   uint32_t off_hver, off_bitmap, off_wpre, off_inptr, off_act, off_list;  // bitmap: 2 x ceil(L/32) words (event parity)
   uint32_t smem_bytes;   // total dynamic smem
@@ -77,6 +78,7 @@ struct Layout {
   uint32_t cluster;      // CTAs per job (thread-block cluster size), 1 = one CTA per job
   uint32_t reg_path;     // 1: every in-degree <= 8 (register ranking path)
   uint32_t worklist;     // 1: compact the destinations with a live in-link before matching
+  uint32_t masked;       // 1: relays (R22): candidates & allow[p], only required arrivals count
 };
 
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,
@@ -88,7 +90,8 @@ int launch_best_keys(const JobOut *d_outs, uint32_t n_seeds, uint32_t seed_offse
                      uint32_t has_rs, uint64_t *d_keys, uint64_t *d_stats, uint64_t *d_times_ag,
                      uint64_t *d_times_rs, void *stream);
 int launch_emit_ag(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
-                   uint64_t shift, void *out_sends, void *stream);
+                   uint64_t shift, void *out_sends, void *stream, uint64_t limit = ~0ull);
+int launch_compact_sends(void *sends, uint64_t n, unsigned long long *d_count, void *stream);
 int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
                         const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
                         size_t scratch_bytes, uint32_t *launches, void *stream, uint32_t mirror = 1,

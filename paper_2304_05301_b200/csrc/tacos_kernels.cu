@@ -56,6 +56,7 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   lay.off_tsrc = o; o += al(L * 4u, 16u);
   lay.off_tw = o; o += al(L * 4u, 16u);
   lay.off_tlid = o; o += al(L * 4u, 16u);
+  lay.off_tdst = o; o += al(L * 4u, 16u);
   lay.off_lv = o; o += al(L, 16u);
   lay.links_bytes = o;
   const uint32_t nbw = (L + 31u) / 32u;
@@ -201,13 +202,15 @@ struct Send32 {
   unsigned long long t0, t1;
 };
 
+// limit: a send ending after it (a relay still in flight when the postcondition
+// holds, R22) is written as a tombstone (chunk = kNone) for compact_sends.
 __global__ void emit_ag_kernel(const Rec *__restrict__ rec, uint64_t M, const uint32_t *__restrict__ src,
                                const uint32_t *__restrict__ dst, const uint32_t *__restrict__ w, uint64_t shift,
-                               Send32 *__restrict__ out) {
+                               uint64_t limit, Send32 *__restrict__ out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < M; i += (uint64_t)gridDim.x * blockDim.x) {
     const Rec r = rec[i];
     Send32 s;
-    s.chunk = r.chunk;
+    s.chunk = r.t_start + w[r.link] > limit ? kNone : r.chunk;
     s.link = r.link;
     s.src = src[r.link];
     s.dst = dst[r.link];
@@ -225,10 +228,48 @@ static int grid_for(uint64_t n, int threads) {
 }
 
 int launch_emit_ag(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
-                   uint64_t shift, void *out_sends, void *stream) {
-  emit_ag_kernel<<<grid_for(M, 256), 256, 0, (cudaStream_t)stream>>>(rec, M, src, dst, w, shift,
+                   uint64_t shift, void *out_sends, void *stream, uint64_t limit) {
+  emit_ag_kernel<<<grid_for(M, 256), 256, 0, (cudaStream_t)stream>>>(rec, M, src, dst, w, shift, limit,
                                                                       reinterpret_cast<Send32 *>(out_sends));
   return check_launch("emit_ag_kernel");
+}
+
+// Stream compaction of the tombstones left by the emitters (relay mode only, R22):
+// one CTA walks the sends tile by tile, order preserved, in place (a kept send
+// moves to an index <= its own, and a tile is read completely before it is written).
+__global__ void compact_sends_kernel(Send32 *__restrict__ s, uint64_t n, unsigned long long *__restrict__ count) {
+  __shared__ uint32_t warp_tot[32];
+  __shared__ unsigned long long base;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (uint64_t t0 = 0; t0 < n; t0 += blockDim.x) {
+    const uint64_t i = t0 + tid;
+    Send32 v{};
+    bool keep = false;
+    if (i < n) {
+      v = s[i];
+      keep = v.chunk != kNone;
+    }
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();  // the whole tile is read (and counted) before any write
+    uint32_t before = 0, total = 0;
+    for (uint32_t j = 0; j < nw; ++j) {
+      before += j < wid ? warp_tot[j] : 0u;
+      total += warp_tot[j];
+    }
+    if (keep) s[base + before + __popc(bal & ((1u << lane) - 1u))] = v;
+    __syncthreads();
+    if (tid == 0) base += total;
+    __syncthreads();
+  }
+  if (tid == 0) *count = base;
+}
+
+int launch_compact_sends(void *sends, uint64_t n, unsigned long long *d_count, void *stream) {
+  compact_sends_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(reinterpret_cast<Send32 *>(sends), n, d_count);
+  return check_launch("compact_sends_kernel");
 }
 
 // RS = mirror of an AG: (c, a->b on l, t0, t1) -> (c, b->a on l', T-t1, T-t0)
@@ -239,8 +280,9 @@ __global__ void rs_keys_kernel(const Rec *__restrict__ rec, uint64_t M, const ui
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < M; i += (uint64_t)gridDim.x * blockDim.x) {
     const Rec r = rec[i];
     const uint32_t l2 = (mirror && rev) ? (uint32_t)rev[r.link] : r.link;
+    const bool late = mirror && r.t_start + w[r.link] > T_rs;  // relay in flight at the end (R22): sorted last
     const unsigned long long t0 = mirror ? T_rs - (r.t_start + w[r.link]) : r.t_start;
-    keys[i] = (t0 << lbits) | l2;
+    keys[i] = late ? ~0ull : ((t0 << lbits) | l2);
     vals[i] = (uint32_t)i;
   }
 }
@@ -253,7 +295,7 @@ __global__ void rs_emit_kernel(const uint32_t *__restrict__ vals, const Rec *__r
     const Rec r = rec[vals[j]];
     const uint32_t l2 = (mirror && rev) ? (uint32_t)rev[r.link] : r.link;
     Send32 s;
-    s.chunk = r.chunk;
+    s.chunk = (mirror && r.t_start + w[r.link] > T_rs) ? kNone : r.chunk;  // tombstone, see rs_keys_kernel
     s.link = l2;
     s.src = src[l2];
     s.dst = dst[l2];

@@ -16,8 +16,10 @@ from typing import List, Optional, Sequence, Tuple
 
 
 def optimum(n: int, links: Sequence[Tuple[int, int, int]], pre: Sequence[int], post: Sequence[int],
-            t_max: int = 32) -> Optional[int]:
+            t_max: int = 32, relays: bool = False) -> Optional[int]:
     """links: (src, dst, w) with integer w >= 1.  pre/post: per-NPU chunk bitmasks.
+    relays=True: a link may also carry a chunk its destination does not require
+    (any relay at all, a superset of the greedy's shortest-path relays, R22).
     Returns the minimum T or None if not reachable within t_max."""
     L = len(links)
     INF = 10 ** 9
@@ -34,6 +36,7 @@ def optimum(n: int, links: Sequence[Tuple[int, int, int]], pre: Sequence[int], p
                     dist[i][j] = dist[i][k] + dist[k][j]
     n_chunks = max((p.bit_length() for p in list(pre) + list(post)), default=0)
     post_t = tuple(post)
+    all_chunks = (1 << n_chunks) - 1
 
     def lower_bound(held, inflight):
         lb = 0
@@ -80,7 +83,7 @@ def optimum(n: int, links: Sequence[Tuple[int, int, int]], pre: Sequence[int], p
             if inflight[l] is not None:
                 options.append([None])
                 continue
-            useful = held[s] & post_t[d] & ~held[d] & ~incoming[d]
+            useful = held[s] & (all_chunks if relays else post_t[d]) & ~held[d] & ~incoming[d]
             opts: List[Optional[int]] = [None]
             c = 0
             while useful:

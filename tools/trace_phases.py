@@ -15,7 +15,7 @@ s = T.synthesize(t, wl.collective, wl.chunks_per_npu, wl.chunk_bytes, wl.n_seeds
 print("T", s.result["T"])
 ''' % (ROOT, cfg)
 names = ["PA", "bar1", "PB", "PM", "bar_pm", "PE-a", "bar2", "PE-b"]
-for q in (1, 2):
+for q in [int(x) for x in os.environ.get("QS", "1,2").split(",")]:
     out = os.path.join(ROOT, "gpurun_out", f"trace_c{cfg}_q{q}.txt")
     env = dict(os.environ, TACOS_CLUSTER=str(q), TACOS_TRACE=out)
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
