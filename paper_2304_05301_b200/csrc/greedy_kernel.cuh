@@ -34,6 +34,8 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "tacos_device.cuh"
 
 namespace tacos {
@@ -89,15 +91,23 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *ord = reinterpret_cast<uint32_t *>(links_base + lay.off_ord);
   uint32_t *pick = reinterpret_cast<uint32_t *>(links_base + lay.off_pick);
   uint32_t *seen = reinterpret_cast<uint32_t *>(links_base + lay.off_seen);
-  uint32_t *order = reinterpret_cast<uint32_t *>(links_base + lay.off_order);
+  uint16_t *order = reinterpret_cast<uint16_t *>(links_base + lay.off_order);  // walk order: position - b0
+  uint16_t *rch = reinterpret_cast<uint16_t *>(links_base + lay.off_rch);      // chunk of a match, 2 event parities
   unsigned char *lv = links_base + lay.off_lv;
-  // per-position topology (source, cost, link id): staged into shared memory with the link state
-  const uint32_t *t_src = p_src, *t_w = p_w, *t_lid = p_lid, *t_dst = T.p_dst;
+  // per-position topology (source, cost, link id, destination): staged into shared memory with
+  // the link state, NPU and link ids as u16 there (the host keeps N, L < 2^16 for that layout)
+  using IdT = typename std::conditional<LINKS_SMEM, uint16_t, uint32_t>::type;
+  const IdT *t_src, *t_lid, *t_dst;
+  const uint32_t *t_w = p_w;
   if constexpr (LINKS_SMEM) {
-    t_src = reinterpret_cast<const uint32_t *>(links_base + lay.off_tsrc);
+    t_src = reinterpret_cast<const IdT *>(links_base + lay.off_tsrc);
     t_w = reinterpret_cast<const uint32_t *>(links_base + lay.off_tw);
-    t_lid = reinterpret_cast<const uint32_t *>(links_base + lay.off_tlid);
-    t_dst = reinterpret_cast<const uint32_t *>(links_base + lay.off_tdst);
+    t_lid = reinterpret_cast<const IdT *>(links_base + lay.off_tlid);
+    t_dst = reinterpret_cast<const IdT *>(links_base + lay.off_tdst);
+  } else {
+    t_src = p_src;
+    t_lid = p_lid;
+    t_dst = T.p_dst;
   }
   uint32_t *hver = reinterpret_cast<uint32_t *>(smem + lay.off_hver);
   uint32_t *bitmap2 = reinterpret_cast<uint32_t *>(smem + lay.off_bitmap);  // 2 x nbw words (event parity)
@@ -155,10 +165,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     cur[p] = kNone;
     seen[p] = kNone;
     if constexpr (LINKS_SMEM) {
-      const_cast<uint32_t *>(t_src)[p] = __ldg(&p_src[p]);
+      const_cast<IdT *>(t_src)[p] = (IdT)__ldg(&p_src[p]);
       const_cast<uint32_t *>(t_w)[p] = __ldg(&p_w[p]);
-      const_cast<uint32_t *>(t_lid)[p] = __ldg(&p_lid[p]);
-      const_cast<uint32_t *>(t_dst)[p] = __ldg(&T.p_dst[p]);
+      const_cast<IdT *>(t_lid)[p] = (IdT)__ldg(&p_lid[p]);
+      const_cast<IdT *>(t_dst)[p] = (IdT)__ldg(&T.p_dst[p]);
     }
   }
   for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) hver[x] = 0u;
@@ -186,19 +196,38 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t ngroups = nthr / P;
   const bool pre_draw = lay.pre_draw != 0u;
   const bool tracing = job.trace != nullptr && tid == 0;
+  // Send records of the matches of event e-1 (own positions, in link-id order of the
+  // event's bitmap, R-records ordered by (t_start, link)): chunk from rch (parity of e-1).
+  auto write_records = [&](uint32_t first, uint32_t stride, uint32_t ev, uint32_t base,
+                           unsigned long long t_start) {
+    if (rec == nullptr || ev == 0u) return;
+    const uint32_t par = (ev + 1u) & 1u;
+    const uint32_t *bmp = bitmap2 + par * nbw;
+    for (uint32_t q = p_lo + first; q < p_hi; q += stride) {
+      const uint32_t lid = t_lid[q];
+      const uint32_t wi = lid >> 5, word = bmp[wi], bit = 1u << (lid & 31u);
+      if (word & bit) {
+        Rec rc;
+        rc.chunk = rch[2u * q + par];
+        rc.link = lid;
+        rc.t_start = t_start;
+        rec[base + wpre[wi] + __popc(word & (bit - 1u))] = rc;
+      }
+    }
+  };
 
   for (;;) {
     long long ts[9];  // debug phase timestamps (TACOS_TRACE), thread 0
     if (tracing) ts[0] = clock64();
     // ================= PA: previous event's records, arrivals at t =================
+    const uint32_t rec_base = s_rec_base;  // record offset of event e-1's matches
     {
-      const uint32_t rec_base = s_rec_base;
-      const uint32_t *bm_prev = bitmap2 + ((e + 1u) & 1u) * nbw;  // bitmap of event e-1
       uint32_t arr = 0;
-      // one thread per in-link position (kPB positions per pass, interleaved for ILP):
-      // the record of the previous event, the arrival (a shared-memory atomicOr on the
-      // destination's held row) and, with pre_draw, the Philox draws of every link free
-      // at t (t and busy_until are fixed here; liveness is decided in PM after the arrivals).
+      // one thread per in-link position (kPB positions per pass, interleaved for ILP): the
+      // arrival (a shared-memory atomicOr on the destination's held row) and, with pre_draw,
+      // the Philox draws of every link free at t (t and busy_until are fixed here; liveness
+      // is decided in PM after the arrivals).  The records of event e-1 are written during
+      // PM (write_records), away from the cluster barrier's fence.
       constexpr int kPB = 4;
       for (uint32_t base = p_lo + tid; base < p_hi; base += nthr * kPB) {
         uint4 r[kPB];
@@ -217,16 +246,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           const unsigned long long b = busy[q];
           const uint32_t c = cur[q];
           if (c != kNone) {
-            if (rec != nullptr && e > 0u && b - t_w[q] == t_prev) {
-              const uint32_t lid = t_lid[q];
-              const uint32_t wi = lid >> 5;
-              const uint32_t idx = rec_base + wpre[wi] + __popc(bm_prev[wi] & ((1u << (lid & 31u)) - 1u));
-              Rec rc;
-              rc.chunk = c;
-              rc.link = lid;
-              rc.t_start = t_prev;
-              rec[idx] = rc;
-            }
             if (b == t) {  // R7: held by dst from this instant
               const uint32_t d = t_dst[q];
               atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
@@ -257,7 +276,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       delivered = 0;
       for (uint32_t r = 0; r < Q; ++r) delivered += s_slot_deliv[r];
     }
-    if (delivered == T.required) break;  // done test (postcondition holds)
+    if (delivered == T.required) {  // done test (postcondition holds)
+      write_records(tid, nthr, e, rec_base, t_prev);  // the last event's matches
+      break;
+    }
     if (tid == 0) s_rec_base = s_next_base;
     ++E;
 
@@ -307,6 +329,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     if (tracing) ts[3] = clock64();
 
     // ================= PM: per-destination draws, order and matching =================
+    // threads beyond the destination groups write the records of event e-1 meanwhile
+    const uint32_t pm_thr = min(nthr, (n_work * P + 31u) & ~31u);
+    if (tid >= pm_thr) write_records(tid - pm_thr, nthr - pm_thr, e, rec_base, t_prev);
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
       for (uint32_t wi = tid / P; wi < n_work; wi += ngroups) {
@@ -408,6 +433,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           if (P > 1) chunk = __shfl_sync(gmask, chunk, __ffs(__ballot_sync(gmask, mine)) - 1);
           if (gl == 0) {
             cur[p] = chunk;
+            rch[2u * p + (e & 1u)] = (uint16_t)chunk;
             busy[p] = t + t_w[p];
             ++myM;
             const uint32_t lid = t_lid[p];
@@ -492,6 +518,145 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) have4[v] = hv[v];
           }
+        } else if constexpr (REG_PATH && P == 2) {
+          // ---- a lane pair per destination: both lanes rank the in-links redundantly
+          //      (no shuffles); the row is split lane-major (lane 0 = chunks [0, C/2),
+          //      lane 1 = the rest, vectors gl*V .. gl*V+V-1), so a step exchanges one
+          //      count; the lane holding the r-th candidate claims it and writes the link ----
+          unsigned long long key[kRegDeg];
+          uint32_t nfree = 0, nlive = 0;
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) {
+            key[j] = ~0ull;
+            if ((uint32_t)j < deg) {
+              const uint32_t q = b0 + (uint32_t)j;
+              const bool isfree = busy[q] <= t;
+              const bool islive = isfree && seen[q] != hver_of(t_src[q]);
+              nfree += isfree ? 1u : 0u;
+              if (islive) {
+                uint32_t o;
+                if (pre_draw) {
+                  o = ord[q];
+                } else {
+                  const uint4 r = philox4x32_10(
+                      make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
+                  o = r.x;
+                  if (gl == 0) pick[q] = r.y;
+                }
+                ++nlive;
+                key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
+              }
+            }
+          }
+          if (gl == 0 && !worklist) {
+            myV += nfree;
+            myD += nfree ? 1u : 0u;
+          }
+          if (nlive == 0u) continue;
+          uint32_t rk[kRegDeg];
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) rk[j] = 0u;
+#pragma unroll
+          for (int i = 0; i < kRegDeg; ++i)
+#pragma unroll
+            for (int j = i + 1; j < kRegDeg; ++j) {
+              const bool jfirst = key[j] < key[i];
+              rk[i] += jfirst ? 1u : 0u;
+              rk[j] += jfirst ? 0u : 1u;
+            }
+          uint32_t ordp = 0;
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
+          auto load_half = [&](uint32_t pp, uint4 (&cv)[V]) {
+            const uint32_t sp = t_src[pp];
+            const bool own_src = Q == 1 || sp - d_lo < d_hi - d_lo;
+            if (!ROWS_SMEM) {
+              const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
+#pragma unroll
+              for (int v = 0; v < V; ++v) cv[v] = __ldcg(&h4[gl * V + v]);
+            } else if (own_src) {
+              const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
+#pragma unroll
+              for (int v = 0; v < V; ++v) cv[v] = h4[gl * V + v];
+            } else {
+              const uint32_t a = dsmem_addr(held + (size_t)sp * Wr, owner_of(sp));
+#pragma unroll
+              for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(gl * V + v) * 16u);
+            }
+          };
+          uint4 hl[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) hl[v] = have4[gl * V + v];
+          uint4 nxt[V];
+          load_half(b0 + (ordp & 15u), nxt);
+          if (!pre_draw) __syncwarp(gmask);  // lane 0's pick draws visible to lane 1
+          for (uint32_t s = 0; s < nlive; ++s) {
+            const uint32_t pp = b0 + ((ordp >> (4u * s)) & 15u);
+            uint4 cv[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) cv[v] = nxt[v];
+            if (s + 1u < nlive) load_half(b0 + ((ordp >> (4u * s + 4u)) & 15u), nxt);
+            uint32_t tot[V], k = 0;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              cv[v] = andnot4(cv[v], hl[v]);  // held[src] & ~have[d], this lane's half
+              if constexpr (MASKED)
+                cv[v] = and4(cv[v], __ldg(reinterpret_cast<const uint4 *>(T.allow + (size_t)pp * Wp) + gl * V + v));
+              tot[v] = popc4(cv[v]);
+              k += tot[v];
+            }
+            const uint32_t ko = __shfl_xor_sync(gmask, k, 1, 2);
+            const uint32_t klo = gl == 0u ? k : ko;  // candidates in the lower half
+            const uint32_t K = k + ko;
+            if (K == 0u) {
+              if (gl == 0u) seen[pp] = hver_of(t_src[pp]);
+              continue;
+            }
+            const uint32_t r = __umulhi(pick[pp], K);  // floor(u_pick * K / 2^32), R13
+            const bool upper = r >= klo;
+            const bool mine = upper == (gl == 1u);
+            uint32_t rv = upper ? r - klo : r;
+            int vsel = 0;
+#pragma unroll
+            for (int v = 0; v + 1 < V; ++v) {
+              const bool adv = (vsel == v) && (rv >= tot[v]);
+              rv = adv ? rv - tot[v] : rv;
+              vsel = adv ? v + 1 : vsel;
+            }
+            uint4 x = cv[0];
+#pragma unroll
+            for (int v = 1; v < V; ++v) x = (vsel == v) ? cv[v] : x;
+            const uint32_t cx = __popc(x.x), cy = __popc(x.y), cz = __popc(x.z);
+            uint32_t rr = rv, wi = 0, word = x.x;
+            bool m = rr >= cx;
+            rr = m ? rr - cx : rr; wi = m ? 1u : wi; word = m ? x.y : word;
+            m = m && rr >= cy;
+            rr = m ? rr - cy : rr; wi = m ? 2u : wi; word = m ? x.z : word;
+            m = m && rr >= cz;
+            rr = m ? rr - cz : rr; wi = m ? 3u : wi; word = m ? x.w : word;
+            const uint32_t bit = select_bit(word, rr);
+            const uint32_t mask = mine ? (1u << bit) : 0u;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              if (vsel == v) {
+                hl[v].x |= wi == 0u ? mask : 0u;
+                hl[v].y |= wi == 1u ? mask : 0u;
+                hl[v].z |= wi == 2u ? mask : 0u;
+                hl[v].w |= wi == 3u ? mask : 0u;
+              }
+            }
+            if (mine) {  // claim (R4): the owning lane writes the link
+              const uint32_t chunk = ((((uint32_t)(gl * V) + (uint32_t)vsel) * 4u + wi) * 32u) + bit;
+              cur[pp] = chunk;
+              rch[2u * pp + (e & 1u)] = (uint16_t)chunk;
+              busy[pp] = t + t_w[pp];
+              ++myM;
+              const uint32_t lid = t_lid[pp];
+              atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) have4[gl * V + v] = hl[v];
         } else if constexpr (REG_PATH) {
           // ---- register path: the group owns the destination's <= kRegDeg in-links, in-link j
           //      in slot j / P of lane j % P; ranks and the walk order stay in registers ----
@@ -633,13 +798,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             // positions of a destination are in ascending link id: u < q <=> lid_u < lid_q
             rank += (wu < wq) || (wu == wq && (ou < oq || (ou == oq && u < q)));
           }
-          order[b0 + rank] = q;
+          order[b0 + rank] = (uint16_t)(q - b0);
         }
         if (P > 1) __syncwarp(gmask);
 #pragma unroll
         for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v * P + gl];
         for (uint32_t s = 0; s < nl; ++s) {
-          const uint32_t p = order[b0 + s];
+          const uint32_t p = b0 + order[b0 + s];
           step(p, pick[p]);
         }
 #pragma unroll
@@ -647,6 +812,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         }
       }
     }
+    if (pm_thr == nthr) write_records(tid, nthr, e, rec_base, t_prev);
     if (tracing) ts[4] = clock64();
     __syncthreads();
     if (tracing) ts[5] = clock64();

@@ -67,7 +67,7 @@ struct Layout {
   uint32_t row_stride;   // words between consecutive rows in shared memory (Wp, padded)
   uint32_t links_bytes;  // per-position arrays
   // within the links region
-  uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv;
+  uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv, off_rch;
   uint32_t off_tsrc, off_tw, off_tlid, off_tdst;  // per-position topology copies (src, w, link id, dst)
   // always in shared memory, after [rows][links] when those are resident
   uint32_t off_hver, off_bitmap, off_wpre, off_inptr, off_act, off_list;  // bitmap: 2 x ceil(L/32) words (event parity)

@@ -52,11 +52,12 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   lay.off_ord = o; o += al(L * 4u, 16u);
   lay.off_pick = o; o += al(L * 4u, 16u);
   lay.off_seen = o; o += al(L * 4u, 16u);
-  lay.off_order = o; o += al(L * 4u, 16u);
-  lay.off_tsrc = o; o += al(L * 4u, 16u);
+  lay.off_order = o; o += al(L * 2u, 16u);   // u16
+  lay.off_rch = o; o += al(L * 4u, 16u);     // u16 x 2 parities
+  lay.off_tsrc = o; o += al(L * 2u, 16u);    // u16 copies (shared-memory layout only)
   lay.off_tw = o; o += al(L * 4u, 16u);
-  lay.off_tlid = o; o += al(L * 4u, 16u);
-  lay.off_tdst = o; o += al(L * 4u, 16u);
+  lay.off_tlid = o; o += al(L * 2u, 16u);
+  lay.off_tdst = o; o += al(L * 2u, 16u);
   lay.off_lv = o; o += al(L, 16u);
   lay.links_bytes = o;
   const uint32_t nbw = (L + 31u) / 32u;
@@ -64,10 +65,11 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   const uint32_t small = al(N * 4u, 16u) + al(2u * nbw * 4u, 16u) + al(nbw * 4u, 16u) + al((N + 1u) * 4u, 16u) +
                          al(2u * act_words * 4u, 16u) + al(N * 4u, 16u);
   const size_t lim = smem_limit;
-  if ((size_t)lay.rows_bytes + lay.links_bytes + small <= lim) {
+  const bool ids16 = N < 65536u && L < 65536u;  // u16 NPU / link ids in the shared-memory link state
+  if ((size_t)lay.rows_bytes + lay.links_bytes + small <= lim && ids16) {
     lay.rows_in_smem = 1;
     lay.links_in_smem = 1;
-  } else if ((size_t)lay.links_bytes + small <= lim) {
+  } else if ((size_t)lay.links_bytes + small <= lim && ids16) {
     lay.rows_in_smem = 0;
     lay.links_in_smem = 1;
   } else {
