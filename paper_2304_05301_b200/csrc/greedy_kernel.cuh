@@ -41,6 +41,9 @@
 namespace tacos {
 
 constexpr int kRegDeg = 8;  // in-degree handled in registers by the P == 1 path
+// P == 1 register path: true = `have` row in shared memory (step_row), false = in registers
+// (the lane-pair path with one lane)
+constexpr bool kP1Smem = true;
 
 template <int V>
 struct ThreadsFor {
@@ -57,7 +60,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   // claim is one word update (no per-word predicated register updates)
   constexpr bool kHaveSmem = (P == 1) && ROWS_SMEM;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long s_min, s_delivered, s_V, s_D, s_M;
+  // 64-bit shared atomics are CAS loops on sm_100a: per-event values use 32-bit atomics
+  // (arrivals of one event; next event time as an offset from t, < 2^32 since w < 2^32)
+  __shared__ unsigned long long s_delivered, s_V, s_D, s_M;
+  __shared__ uint32_t s_arr[2], s_min32;
   // cluster exchange slots, indexed by the writer's rank (plain remote stores, no 64-bit DSMEM atomics)
   __shared__ unsigned long long s_slot_deliv[8], s_slot_min[8], s_slot_cnt[8][3];
   __shared__ uint32_t s_rec_base, s_next_base;
@@ -116,6 +122,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *s_act = reinterpret_cast<uint32_t *>(smem + lay.off_act);      // worklist bitmaps (2 x act_words)
   uint32_t *s_list = reinterpret_cast<uint32_t *>(smem + lay.off_list);    // worklist entries
   __shared__ uint32_t s_nwork;
+  __shared__ unsigned s_dbg[2];  // debug (TACOS_TRACE): slowest matching / record thread of an event
+  if (tid < 2) s_dbg[tid] = 0u;
   const uint32_t nbw = (L + 31u) / 32u;
   const uint32_t seed_lo = (uint32_t)job.seed, seed_hi = (uint32_t)(job.seed >> 32);
   Rec *rec = job.rec;
@@ -178,10 +186,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;
   if (tid == 0) {
     s_delivered = 0ull;
+    s_arr[0] = s_arr[1] = 0u;
+    s_min32 = ~0u;
     s_V = s_D = s_M = 0ull;
     s_rec_base = 0u;
     s_next_base = 0u;
-    s_min = ~0ull;
   }
   (void)NW;
   cluster_barrier();  // peers may read our rows / add to our counters from now on
@@ -216,6 +225,34 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
   };
 
+  // pre_draw: Philox draws (R2) of every own link free at time tq, made ahead of the
+  // event (t and busy_until are fixed by then; liveness is decided in PM after the
+  // arrivals), kPB positions per pass so the Philox chains interleave.
+  auto draw_ahead = [&](unsigned long long tq, uint32_t first, uint32_t stride) {
+    constexpr int kPB = 4;
+    for (uint32_t base = p_lo + first; base < p_hi; base += stride * kPB) {
+      uint4 r[kPB];
+#pragma unroll
+      for (int u = 0; u < kPB; ++u) {
+        const uint32_t q = base + (uint32_t)u * stride;
+        r[u] = philox4x32_10(make_uint4((uint32_t)tq, (uint32_t)(tq >> 32), q < p_hi ? (uint32_t)t_lid[q] : 0u,
+                                        job.sigma), seed_lo, seed_hi);
+      }
+#pragma unroll
+      for (int u = 0; u < kPB; ++u) {
+        const uint32_t q = base + (uint32_t)u * stride;
+        if (q < p_hi && busy[q] <= tq) {
+          ord[q] = r[u].x;
+          pick[q] = r[u].y;
+        }
+      }
+    }
+  };
+  if (pre_draw) {  // the draws of the first event (t = 0: every link is free)
+    __syncthreads();
+    draw_ahead(0ull, tid, nthr);
+  }
+
   for (;;) {
     long long ts[9];  // debug phase timestamps (TACOS_TRACE), thread 0
     if (tracing) ts[0] = clock64();
@@ -223,55 +260,32 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     const uint32_t rec_base = s_rec_base;  // record offset of event e-1's matches
     {
       uint32_t arr = 0;
-      // one thread per in-link position (kPB positions per pass, interleaved for ILP): the
-      // arrival (a shared-memory atomicOr on the destination's held row) and, with pre_draw,
-      // the Philox draws of every link free at t (t and busy_until are fixed here; liveness
-      // is decided in PM after the arrivals).  The records of event e-1 are written during
-      // PM (write_records), away from the cluster barrier's fence.
-      constexpr int kPB = 4;
-      for (uint32_t base = p_lo + tid; base < p_hi; base += nthr * kPB) {
-        uint4 r[kPB];
-        if (pre_draw) {
-#pragma unroll
-          for (int u = 0; u < kPB; ++u) {
-            const uint32_t q = base + (uint32_t)u * nthr;
-            r[u] = philox4x32_10(make_uint4((uint32_t)t, (uint32_t)(t >> 32), q < p_hi ? t_lid[q] : 0u, job.sigma),
-                                 seed_lo, seed_hi);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kPB; ++u) {
-          const uint32_t q = base + (uint32_t)u * nthr;
-          if (q >= p_hi) break;
-          const unsigned long long b = busy[q];
-          const uint32_t c = cur[q];
-          if (c != kNone) {
-            if (b == t) {  // R7: held by dst from this instant
-              const uint32_t d = t_dst[q];
-              atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
-              hver[d] = e;
-              cur[q] = kNone;
-              // a relayed chunk (not in post[d]) is held but not required
-              if (!MASKED || ((__ldg(&T.post[(size_t)d * Wp + (c >> 5)]) >> (c & 31u)) & 1u)) ++arr;
-            }
-          }
-          if (pre_draw && b <= t) {
-            ord[q] = r[u].x;
-            pick[q] = r[u].y;
-          }
+      // one thread per in-link position: the arrival (a shared-memory atomicOr on the
+      // destination's held row).  With pre_draw the Philox draws of this event were made
+      // at the end of the previous one (draw_ahead); the records of event e-1 are written
+      // during PM (write_records), away from the cluster barrier's fence.
+      for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
+        const uint32_t c = cur[q];
+        if (c != kNone && busy[q] == t) {  // R7: held by dst from this instant
+          const uint32_t d = t_dst[q];
+          atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
+          hver[d] = e;
+          cur[q] = kNone;
+          // a relayed chunk (not in post[d]) is held but not required
+          if (!MASKED || ((__ldg(&T.post[(size_t)d * Wp + (c >> 5)]) >> (c & 31u)) & 1u)) ++arr;
         }
       }
       arr = warp_sum_u32(arr);
-      if (lane == 0 && arr) atomicAdd(&s_delivered, (unsigned long long)arr);  // own deliveries, cumulative
+      if (lane == 0 && arr) atomicAdd(&s_arr[e & 1u], arr);  // own deliveries of this event
       if (Q > 1) {
         __syncthreads();
-        if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_deliv[crank], tid), s_delivered);
+        if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_deliv[crank], tid), s_delivered + s_arr[e & 1u]);
       }
     }
     if (tracing) ts[1] = clock64();
     cluster_barrier();
     if (tracing) ts[2] = clock64();
-    unsigned long long delivered = s_delivered;
+    unsigned long long delivered = s_delivered + s_arr[e & 1u];  // own, cumulative
     if (Q > 1) {
       delivered = 0;
       for (uint32_t r = 0; r < Q; ++r) delivered += s_slot_deliv[r];
@@ -331,7 +345,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     // ================= PM: per-destination draws, order and matching =================
     // threads beyond the destination groups write the records of event e-1 meanwhile
     const uint32_t pm_thr = min(nthr, (n_work * P + 31u) & ~31u);
-    if (tid >= pm_thr) write_records(tid - pm_thr, nthr - pm_thr, e, rec_base, t_prev);
+    const long long pm_t0 = job.trace != nullptr ? clock64() : 0;  // debug: slowest thread of the phase
+    if (tid >= pm_thr) {
+      write_records(tid - pm_thr, nthr - pm_thr, e, rec_base, t_prev);
+      if (job.trace != nullptr) atomicMax(&s_dbg[1], (unsigned)(clock64() - pm_t0));
+    }
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
       for (uint32_t wi = tid / P; wi < n_work; wi += ngroups) {
@@ -448,7 +466,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         };
 
         // REG_PATH (every in-degree <= kRegDeg): ranks in registers; else shared memory
-        if constexpr (REG_PATH && P == 1) {
+        if constexpr (REG_PATH && P == 1 && kP1Smem) {
           // ---- one thread per destination: in-link j in slot j (static), ranks by the
           //      28 pairwise comparisons, walk order packed 4 bits per rank, and the
           //      next in-link's source row loaded while the current one is matched ----
@@ -518,11 +536,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) have4[v] = hv[v];
           }
-        } else if constexpr (REG_PATH && P == 2) {
-          // ---- a lane pair per destination: both lanes rank the in-links redundantly
-          //      (no shuffles); the row is split lane-major (lane 0 = chunks [0, C/2),
-          //      lane 1 = the rest, vectors gl*V .. gl*V+V-1), so a step exchanges one
-          //      count; the lane holding the r-th candidate claims it and writes the link ----
+        } else if constexpr (REG_PATH && P <= 2) {
+          // ---- a group of P lanes per destination: every lane ranks the in-links itself
+          //      (redundant, no shuffles); the row is split lane-major (lane gl holds the
+          //      vectors gl*V .. gl*V+V-1, chunks in ascending order across the lanes), so a
+          //      step needs one inclusive scan of the lane counts; the lane holding the r-th
+          //      candidate claims it and writes the link; the next in-link's row is loaded
+          //      while the current one is matched ----
           unsigned long long key[kRegDeg];
           uint32_t nfree = 0, nlive = 0;
 #pragma unroll
@@ -605,17 +625,21 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               tot[v] = popc4(cv[v]);
               k += tot[v];
             }
-            const uint32_t ko = __shfl_xor_sync(gmask, k, 1, 2);
-            const uint32_t klo = gl == 0u ? k : ko;  // candidates in the lower half
-            const uint32_t K = k + ko;
+            uint32_t incl = k;  // inclusive scan of the lane counts over the group
+#pragma unroll
+            for (int o = 1; o < P; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(gmask, incl, o, P);
+              if (gl >= (uint32_t)o) incl += y;
+            }
+            const uint32_t K = P > 1 ? __shfl_sync(gmask, incl, P - 1, P) : incl;
             if (K == 0u) {
               if (gl == 0u) seen[pp] = hver_of(t_src[pp]);
               continue;
             }
             const uint32_t r = __umulhi(pick[pp], K);  // floor(u_pick * K / 2^32), R13
-            const bool upper = r >= klo;
-            const bool mine = upper == (gl == 1u);
-            uint32_t rv = upper ? r - klo : r;
+            const uint32_t excl = incl - k;
+            const bool mine = r >= excl && r < incl;
+            uint32_t rv = r - excl;
             int vsel = 0;
 #pragma unroll
             for (int v = 0; v + 1 < V; ++v) {
@@ -658,7 +682,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
           for (int v = 0; v < V; ++v) have4[gl * V + v] = hl[v];
         } else if constexpr (REG_PATH) {
-          // ---- register path: the group owns the destination's <= kRegDeg in-links, in-link j
+          // ---- register path for wide rows (P > 2, measured faster there than the lane-major
+          //      group path): the group owns the destination's <= kRegDeg in-links, in-link j
           //      in slot j / P of lane j % P; ranks and the walk order stay in registers ----
           constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
           unsigned long long key[SL];
@@ -812,10 +837,15 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         }
       }
     }
+    if (job.trace != nullptr && tid < pm_thr) atomicMax(&s_dbg[0], (unsigned)(clock64() - pm_t0));
     if (pm_thr == nthr) write_records(tid, nthr, e, rec_base, t_prev);
     if (tracing) ts[4] = clock64();
     __syncthreads();
     if (tracing) ts[5] = clock64();
+    if (tid == 0) {  // every thread has read this event's arrivals (done test, publication)
+      s_delivered += s_arr[e & 1u];
+      s_arr[e & 1u] = 0u;
+    }
 
     // ================= PE: next event time, record offsets =================
     {
@@ -837,15 +867,22 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           mn = b < mn ? b : mn;
         }
       mn = warp_min_u64(mn);
-      if (lane == 0 && mn != ~0ull) atomicMin(&s_min, mn);  // own positions
+      if (lane == 0 && mn != ~0ull) atomicMin(&s_min32, (uint32_t)(mn - t));  // own positions, offset from t
       if (Q > 1) {
         __syncthreads();
-        if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid), s_min);
+        if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid), s_min32 == ~0u ? ~0ull : t + s_min32);
       }
       if (tracing) ts[6] = clock64();
       cluster_barrier();
       if (tracing) ts[7] = clock64();
-      // (b) record offsets of this event from the combined bitmap
+      // (b) record offsets of this event from the combined bitmap (warp 0); the other
+      // warps draw ahead for the next event meanwhile
+      if (pre_draw && tid >= 32u) {
+        unsigned long long tq = s_min32 == ~0u ? ~0ull : t + s_min32;
+        if (Q > 1)
+          for (uint32_t r = 0; r < Q; ++r) tq = s_slot_min[r] < tq ? s_slot_min[r] : tq;
+        if (tq != ~0ull) draw_ahead(tq, tid - 32u, nthr - 32u);
+      }
       if (tid < 32) {
         uint32_t running = 0;
         for (uint32_t base = 0; base < nbw; base += 32u) {
@@ -866,7 +903,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       if (worklist)
         for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;  // consumed by this event's PM
     }
-    unsigned long long tn = s_min;
+    unsigned long long tn = s_min32 == ~0u ? ~0ull : t + s_min32;
     if (Q > 1)
       for (uint32_t r = 0; r < Q; ++r) tn = s_slot_min[r] < tn ? s_slot_min[r] : tn;
     __syncthreads();  // wpre / s_next_base ready; everyone has read s_min
@@ -878,8 +915,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       tr[2] = tn;
       tr[3] = s_next_base - s_rec_base;
       for (int i = 1; i < 9; ++i) tr[3 + i] = (unsigned long long)(ts[i] - ts[i - 1]);
+      tr[12] = s_dbg[0];
+      tr[13] = s_dbg[1];
+      s_dbg[0] = s_dbg[1] = 0u;
     }
-    if (tid == 0) s_min = ~0ull;  // own-position minimum of the next event
+    if (tid == 0) s_min32 = ~0u;  // own-position minimum of the next event
     if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)
       status = -3;
       break;

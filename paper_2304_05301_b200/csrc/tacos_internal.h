@@ -52,7 +52,7 @@ struct Job {
   unsigned long long *trace;  // debug (TACOS_TRACE): per CTA rank, per event {t, delivered, local min, matches}
 };
 constexpr uint32_t kTraceEvents = 4096;
-constexpr uint32_t kTraceWords = 12;  // t, delivered, t_next, matches, 8 phase durations (clock64)
+constexpr uint32_t kTraceWords = 14;  // t, delivered, t_next, matches, 8 phase durations, slowest PM / record thread
 
 struct JobOut {
   uint64_t T, V, D, M, E;

@@ -104,7 +104,8 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   }
   lay.cluster = Q;
   const uint32_t n_own = (N + Q - 1) / Q;
-  lay.pre_draw = (n_own * P * 2u <= th) ? 1u : 0u;  // destination groups would leave half the threads idle
+  lay.pre_draw = 0u;  // 1: draws made ahead in the previous event's record-offset phase (measured slower)
+  (void)n_own;
   if (const char *env = getenv("TACOS_PRE_DRAW")) lay.pre_draw = (uint32_t)atoi(env);
   return lay;
 }

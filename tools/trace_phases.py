@@ -27,4 +27,6 @@ for q in [int(x) for x in os.environ.get("QS", "1,2").split(",")]:
         tot = [sum(x[6 + i] for x in rr) for i in range(8)]
         all_ = sum(tot)
         print(f"  rank {rank}: events {n}, cycles/event {all_ / n:.0f}: " +
-              " ".join(f"{nm}={tot[i] / n:.0f}" for i, nm in enumerate(names)))
+              " ".join(f"{nm}={tot[i] / n:.0f}" for i, nm in enumerate(names)) +
+              (f" | slowest PM thread {sum(x[14] for x in rr) / n:.0f} record thread {sum(x[15] for x in rr) / n:.0f}"
+               if len(rr[0]) > 15 else ""))
