@@ -135,55 +135,64 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
                                  uint32_t rs_base, uint32_t has_rs, unsigned long long *keys,
                                  unsigned long long *stats, unsigned long long *times_ag,
                                  unsigned long long *times_rs) {
-  __shared__ unsigned long long s_k0, s_k1, s_V, s_D, s_M, s_E, s_X;
-  __shared__ int s_status;
-  if (threadIdx.x == 0) {
-    s_k0 = s_k1 = kNoKey;
-    s_V = s_D = s_M = s_E = s_X = 0ull;
-    s_status = 0;
-  }
-  __syncthreads();
+  // per-thread partials -> warp shuffles -> one slot per warp -> warp 0 (64-bit shared
+  // atomics would be CAS loops on sm_100a)
+  constexpr int kVals = 7;  // k0, k1 (min); V, D, M, E, X (sum)
+  __shared__ unsigned long long s_w[32][kVals];
+  __shared__ int s_st[32];
   const uint32_t n_jobs = has_rs ? rs_base + n_seeds : n_seeds;
-  unsigned long long k0 = kNoKey, k1 = kNoKey, V = 0, D = 0, M = 0, E = 0, X = 0;
+  unsigned long long v[kVals] = {kNoKey, kNoKey, 0ull, 0ull, 0ull, 0ull, 0ull};
   int st = 0;
   for (uint32_t j = threadIdx.x; j < n_jobs; j += blockDim.x) {
     const JobOut o = outs[j];
-    V += o.V;
-    D += o.D;
-    M += o.M;
-    E += o.E;
-    X += o.pad;
-    if (o.status != 0) st = o.status;
+    v[2] += o.V;
+    v[3] += o.D;
+    v[4] += o.M;
+    v[5] += o.E;
+    v[6] += o.pad;
+    if (o.status != 0) st = min(st, o.status);
     const bool is_rs = has_rs && j >= rs_base;
     const uint32_t i = is_rs ? j - rs_base : j;
     const unsigned long long key =
         o.status == 0 ? ((o.T << kKeySeedBits) | (unsigned long long)(seed_offset + i)) : kNoKey;
     if (is_rs) {
-      k1 = key < k1 ? key : k1;
+      v[1] = key < v[1] ? key : v[1];
       if (times_rs) times_rs[i] = o.T;
     } else {
-      k0 = key < k0 ? key : k0;
+      v[0] = key < v[0] ? key : v[0];
       if (times_ag) times_ag[i] = o.T;
     }
   }
-  atomicMin(&s_k0, k0);
-  atomicMin(&s_k1, k1);
-  atomicAdd(&s_V, V);
-  atomicAdd(&s_D, D);
-  atomicAdd(&s_M, M);
-  atomicAdd(&s_E, E);
-  atomicAdd(&s_X, X);
-  if (st != 0) atomicMin(&s_status, st);
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5, nw = (blockDim.x + 31u) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < kVals; ++q) {
+      const unsigned long long y = __shfl_xor_sync(0xFFFFFFFFu, v[q], o);
+      v[q] = q < 2 ? (y < v[q] ? y : v[q]) : v[q] + y;
+    }
+    st = min(st, __shfl_xor_sync(0xFFFFFFFFu, st, o));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kVals; ++q) s_w[wid][q] = v[q];
+    s_st[wid] = st;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    keys[0] = s_k0;
-    keys[1] = has_rs ? s_k1 : s_k0;
-    stats[0] = s_V;
-    stats[1] = s_D;
-    stats[2] = s_M;
-    stats[3] = s_E;
-    stats[4] = (unsigned long long)(long long)s_status;
-    stats[5] = s_X;
+    for (uint32_t w = 1; w < nw; ++w) {
+#pragma unroll
+      for (int q = 0; q < kVals; ++q) v[q] = q < 2 ? (s_w[w][q] < v[q] ? s_w[w][q] : v[q]) : v[q] + s_w[w][q];
+      st = min(st, s_st[w]);
+    }
+    keys[0] = v[0];
+    keys[1] = has_rs ? v[1] : v[0];
+    stats[0] = v[2];
+    stats[1] = v[3];
+    stats[2] = v[4];
+    stats[3] = v[5];
+    stats[4] = (unsigned long long)(long long)st;
+    stats[5] = v[6];
   }
 }
 
