@@ -169,6 +169,10 @@ class ClockSampler:
             return
         self.thr = threading.Thread(target=self._read, daemon=True)
         self.thr.start()
+        t_end = time.time() + 5.0  # nvidia-smi start-up (slow with several ranks): wait for the first sample
+        while not self.lines and time.time() < t_end and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.lines.clear()  # keep only the samples taken from here on (the timed region)
 
     def _read(self):
         for line in self.proc.stdout:
