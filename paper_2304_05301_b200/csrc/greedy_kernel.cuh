@@ -63,10 +63,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   // 64-bit shared atomics are CAS loops on sm_100a: per-event values use 32-bit atomics
   // (arrivals of one event; next event time as an offset from t, < 2^32 since w < 2^32)
   __shared__ unsigned long long s_delivered, s_V, s_D, s_M;
-  __shared__ uint32_t s_arr[2], s_min32;
+  __shared__ uint32_t s_arr[2], s_min32[2], s_mcnt[2];
   // cluster exchange slots, indexed by the writer's rank (plain remote stores, no 64-bit DSMEM atomics)
   __shared__ unsigned long long s_slot_deliv[8], s_slot_min[8], s_slot_cnt[8][3];
-  __shared__ uint32_t s_rec_base, s_next_base;
 
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -187,10 +186,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   if (tid == 0) {
     s_delivered = 0ull;
     s_arr[0] = s_arr[1] = 0u;
-    s_min32 = ~0u;
     s_V = s_D = s_M = 0ull;
-    s_rec_base = 0u;
-    s_next_base = 0u;
   }
   (void)NW;
   cluster_barrier();  // peers may read our rows / add to our counters from now on
@@ -205,14 +201,37 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t ngroups = nthr / P;
   const bool pre_draw = lay.pre_draw != 0u;
   const bool tracing = job.trace != nullptr && tid == 0;
-  // Send records of the matches of event e-1 (own positions, in link-id order of the
-  // event's bitmap, R-records ordered by (t_start, link)): chunk from rch (parity of e-1).
-  auto write_records = [&](uint32_t first, uint32_t stride, uint32_t ev, uint32_t base,
-                           unsigned long long t_start) {
+  // Send records of the matches of event ev-1 (own positions; their index = base + rank of
+  // the link id in the cluster-wide bitmap of ev-1, so records are ordered by (t_start, link)),
+  // chunk from rch (parity of ev-1), by a group of `count` threads starting at `first` (a
+  // multiple of 32; the whole CTA when first == 0): the group's first warp turns the bitmap
+  // into word offsets, the group writes, then clears the bitmap for its reuse at ev+1.
+  auto write_records = [&](uint32_t first, uint32_t count, uint32_t ev, uint32_t base,
+                           unsigned long long t_start, bool clear) {
     if (rec == nullptr || ev == 0u) return;
+    auto group_sync = [&]() {
+      if (count == nthr) __syncthreads();
+      else asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory");
+    };
     const uint32_t par = (ev + 1u) & 1u;
-    const uint32_t *bmp = bitmap2 + par * nbw;
-    for (uint32_t q = p_lo + first; q < p_hi; q += stride) {
+    uint32_t *bmp = bitmap2 + par * nbw;
+    if (tid - first < 32u) {
+      uint32_t running = 0;
+      for (uint32_t b = 0; b < nbw; b += 32u) {
+        const uint32_t i = b + lane;
+        const uint32_t v = i < nbw ? __popc(bmp[i]) : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        if (i < nbw) wpre[i] = running + incl - v;
+        running += __shfl_sync(0xFFFFFFFFu, incl, 31);
+      }
+    }
+    group_sync();
+    for (uint32_t q = p_lo + (tid - first); q < p_hi; q += count) {
       const uint32_t lid = t_lid[q];
       const uint32_t wi = lid >> 5, word = bmp[wi], bit = 1u << (lid & 31u);
       if (word & bit) {
@@ -223,7 +242,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         rec[base + wpre[wi] + __popc(word & (bit - 1u))] = rc;
       }
     }
+    if (clear) {
+      group_sync();
+      for (uint32_t i = tid - first; i < nbw; i += count) bmp[i] = 0u;
+    }
   };
+  uint32_t rb = 0, rb_prev = 0;  // record offsets of the matches of events e and e-1 (cluster-wide)
 
   // pre_draw: Philox draws (R2) of every own link free at time tq, made ahead of the
   // event (t and busy_until are fixed by then; liveness is decided in PM after the
@@ -256,8 +280,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   for (;;) {
     long long ts[9];  // debug phase timestamps (TACOS_TRACE), thread 0
     if (tracing) ts[0] = clock64();
-    // ================= PA: previous event's records, arrivals at t =================
-    const uint32_t rec_base = s_rec_base;  // record offset of event e-1's matches
+    // ================= PA: arrivals at t =================
+    if (tid == 0) {  // this event's counters (their parity was last read two events ago)
+      s_min32[e & 1u] = ~0u;
+      s_mcnt[e & 1u] = 0u;
+    }
+    if (worklist)
+      for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;
     {
       uint32_t arr = 0;
       // one thread per in-link position: the arrival (a shared-memory atomicOr on the
@@ -291,10 +320,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       for (uint32_t r = 0; r < Q; ++r) delivered += s_slot_deliv[r];
     }
     if (delivered == T.required) {  // done test (postcondition holds)
-      write_records(tid, nthr, e, rec_base, t_prev);  // the last event's matches
+      write_records(0u, nthr, e, rb_prev, t_prev, false);  // the last event's matches
       break;
     }
-    if (tid == 0) s_rec_base = s_next_base;
     ++E;
 
     // ================= PW (optional): worklist of destinations with a live in-link =================
@@ -346,8 +374,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     // threads beyond the destination groups write the records of event e-1 meanwhile
     const uint32_t pm_thr = min(nthr, (n_work * P + 31u) & ~31u);
     const long long pm_t0 = job.trace != nullptr ? clock64() : 0;  // debug: slowest thread of the phase
+    uint32_t my_claims = 0;  // this event's matches of this thread (published with the next time)
     if (tid >= pm_thr) {
-      write_records(tid - pm_thr, nthr - pm_thr, e, rec_base, t_prev);
+      write_records(pm_thr, nthr - pm_thr, e, rb_prev, t_prev, true);
       if (job.trace != nullptr) atomicMax(&s_dbg[1], (unsigned)(clock64() - pm_t0));
     }
     {
@@ -454,6 +483,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             rch[2u * p + (e & 1u)] = (uint16_t)chunk;
             busy[p] = t + t_w[p];
             ++myM;
+            ++my_claims;
             const uint32_t lid = t_lid[p];
             atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
           }
@@ -675,6 +705,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               rch[2u * pp + (e & 1u)] = (uint16_t)chunk;
               busy[pp] = t + t_w[pp];
               ++myM;
+              ++my_claims;
               const uint32_t lid = t_lid[pp];
               atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
             }
@@ -838,7 +869,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       }
     }
     if (job.trace != nullptr && tid < pm_thr) atomicMax(&s_dbg[0], (unsigned)(clock64() - pm_t0));
-    if (pm_thr == nthr) write_records(tid, nthr, e, rec_base, t_prev);
+    if (pm_thr == nthr) write_records(0u, nthr, e, rb_prev, t_prev, true);
+    my_claims = __reduce_add_sync(0xFFFFFFFFu, my_claims);
+    if (lane == 0 && my_claims) atomicAdd(&s_mcnt[e & 1u], my_claims);
     if (tracing) ts[4] = clock64();
     __syncthreads();
     if (tracing) ts[5] = clock64();
@@ -847,11 +880,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       s_arr[e & 1u] = 0u;
     }
 
-    // ================= PE: next event time, record offsets =================
+    // ================= PE: next event time, this event's match count =================
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
-      uint32_t *bm_clear = bitmap2 + ((e + 1u) & 1u) * nbw;  // event e-1's map: its records are written
-      // (a) publish: own matched links into the peers' bitmaps, own min busy_until everywhere
+      // publish: own matched links into the peers' bitmaps; own min busy_until (as an offset
+      // from t, < 2^32) and own match count into every CTA's slot
       if (Q > 1) {
         for (uint32_t i = tid; i < nbw; i += nthr) {
           const uint32_t wbits = bm[i];
@@ -860,66 +893,49 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               if (r != crank) dsmem_or_b32(dsmem_addr(bm + i, r), wbits);
         }
       }
-      unsigned long long mn = ~0ull;
+      uint32_t mo = ~0u;
       for (uint32_t p = p_lo + tid; p < p_hi; p += nthr)
         if (cur[p] != kNone) {
-          const unsigned long long b = busy[p];
-          mn = b < mn ? b : mn;
+          const uint32_t o = (uint32_t)(busy[p] - t);
+          mo = o < mo ? o : mo;
         }
-      mn = warp_min_u64(mn);
-      if (lane == 0 && mn != ~0ull) atomicMin(&s_min32, (uint32_t)(mn - t));  // own positions, offset from t
-      if (Q > 1) {
-        __syncthreads();
-        if (tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid), s_min32 == ~0u ? ~0ull : t + s_min32);
-      }
+      mo = __reduce_min_sync(0xFFFFFFFFu, mo);
+      if (lane == 0 && mo != ~0u) atomicMin(&s_min32[e & 1u], mo);
+      __syncthreads();
+      if (Q > 1 && tid < Q)
+        dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid),
+                     ((unsigned long long)s_min32[e & 1u] << 32) | s_mcnt[e & 1u]);
       if (tracing) ts[6] = clock64();
-      cluster_barrier();
+      if (Q > 1) cluster.sync();
       if (tracing) ts[7] = clock64();
-      // (b) record offsets of this event from the combined bitmap (warp 0); the other
-      // warps draw ahead for the next event meanwhile
-      if (pre_draw && tid >= 32u) {
-        unsigned long long tq = s_min32 == ~0u ? ~0ull : t + s_min32;
-        if (Q > 1)
-          for (uint32_t r = 0; r < Q; ++r) tq = s_slot_min[r] < tq ? s_slot_min[r] : tq;
-        if (tq != ~0ull) draw_ahead(tq, tid - 32u, nthr - 32u);
-      }
-      if (tid < 32) {
-        uint32_t running = 0;
-        for (uint32_t base = 0; base < nbw; base += 32u) {
-          const uint32_t i = base + lane;
-          const uint32_t v = i < nbw ? __popc(bm[i]) : 0u;
-          uint32_t incl = v;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= (uint32_t)o) incl += y;
-          }
-          if (i < nbw) wpre[i] = running + incl - v;
-          running += __shfl_sync(0xFFFFFFFFu, incl, 31);
-        }
-        if (lane == 0) s_next_base = s_rec_base + running;
-      }
-      for (uint32_t i = tid; i < nbw; i += nthr) bm_clear[i] = 0u;
-      if (worklist)
-        for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;  // consumed by this event's PM
     }
-    unsigned long long tn = s_min32 == ~0u ? ~0ull : t + s_min32;
-    if (Q > 1)
-      for (uint32_t r = 0; r < Q; ++r) tn = s_slot_min[r] < tn ? s_slot_min[r] : tn;
-    __syncthreads();  // wpre / s_next_base ready; everyone has read s_min
+    uint32_t mo_all = s_min32[e & 1u], m_all = s_mcnt[e & 1u];
+    if (Q > 1) {
+      mo_all = ~0u;
+      m_all = 0u;
+      for (uint32_t r = 0; r < Q; ++r) {
+        const unsigned long long v = s_slot_min[r];
+        const uint32_t hi = (uint32_t)(v >> 32);
+        mo_all = hi < mo_all ? hi : mo_all;
+        m_all += (uint32_t)v;
+      }
+    }
+    const unsigned long long tn = mo_all == ~0u ? ~0ull : t + mo_all;
+    rb_prev = rb;
+    rb += m_all;
+    if (pre_draw && tn != ~0ull) draw_ahead(tn, tid, nthr);  // (optional) the next event's draws
     if (tracing && e < kTraceEvents) {
       ts[8] = clock64();
       unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e) * kTraceWords;
       tr[0] = t;
       tr[1] = delivered;
       tr[2] = tn;
-      tr[3] = s_next_base - s_rec_base;
+      tr[3] = m_all;
       for (int i = 1; i < 9; ++i) tr[3 + i] = (unsigned long long)(ts[i] - ts[i - 1]);
       tr[12] = s_dbg[0];
       tr[13] = s_dbg[1];
       s_dbg[0] = s_dbg[1] = 0u;
     }
-    if (tid == 0) s_min32 = ~0u;  // own-position minimum of the next event
     if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)
       status = -3;
       break;
