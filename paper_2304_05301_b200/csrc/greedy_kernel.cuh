@@ -121,8 +121,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *s_act = reinterpret_cast<uint32_t *>(smem + lay.off_act);      // worklist bitmaps (2 x act_words)
   uint32_t *s_list = reinterpret_cast<uint32_t *>(smem + lay.off_list);    // worklist entries
   __shared__ uint32_t s_nwork;
-  __shared__ unsigned s_dbg[2];  // debug (TACOS_TRACE): slowest matching / record thread of an event
-  if (tid < 2) s_dbg[tid] = 0u;
+  __shared__ unsigned s_dbg[5];  // debug (TACOS_TRACE): slowest matching / record thread of an event
+  if (tid < 5) s_dbg[tid] = 0u;
   const uint32_t nbw = (L + 31u) / 32u;
   const uint32_t seed_lo = (uint32_t)job.seed, seed_hi = (uint32_t)(job.seed >> 32);
   Rec *rec = job.rec;
@@ -141,15 +141,19 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   // exact while x * (m * chunkN - 2^32) < 2^32, i.e. for N < 2^16
   const uint32_t own_magic = (uint32_t)((0xFFFFFFFFull + chunkN) / chunkN);
   auto owner_of = [&](uint32_t x) -> uint32_t { return N < 65536u ? __umulhi(x, own_magic) : x / chunkN; };
-  // source version of NPU x (owned by CTA owner_of(x))
-  auto hver_of = [&](uint32_t x) -> uint32_t {
-    if (Q == 1 || x - d_lo < d_hi - d_lo) return hver[x];  // own NPU (the common case)
-    return dsmem_ld(dsmem_addr(hver + x, owner_of(x)));
-  };
+  // Mirrors: a CTA keeps local copies of the held rows (shared-memory layout) and source
+  // versions of the peers' NPUs that are sources of its in-links; the owner pushes every
+  // arrival to them (DSMEM red.or / st) before the cluster barrier, so the matching phase
+  // reads only its own shared memory.  s_peers[x] (own x): peer ranks that mirror x.
+  uint32_t *s_peers = reinterpret_cast<uint32_t *>(smem + lay.off_peers);
+  auto hver_of = [&](uint32_t x) -> uint32_t { return hver[x]; };
 
   // ---- a2: state init (P:L89 precondition; P:L212 start at t = 0) ----
   const uint32_t NW = N * Wp;
-  for (uint32_t i = d_lo * Wp + tid; i < d_hi * Wp; i += nthr) {
+  // held: every row in shared memory (own rows and the mirrors), own rows only in global memory
+  // (shared by the cluster); have: own rows
+  const uint32_t i_lo = ROWS_SMEM ? 0u : d_lo * Wp, i_hi = ROWS_SMEM ? NW : d_hi * Wp;
+  for (uint32_t i = i_lo + tid; i < i_hi; i += nthr) {
     uint32_t v, hv0;
     const uint32_t x = i / Wp, q = i - x * Wp;
     if (custom) {
@@ -165,7 +169,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       hv0 = v;
     }
     held[(size_t)x * Wr + q] = v;
-    have[(size_t)x * Wr + q] = hv0;
+    if (x - d_lo < d_hi - d_lo) have[(size_t)x * Wr + q] = hv0;
   }
   for (uint32_t p = p_lo + tid; p < p_hi; p += nthr) {
     busy[p] = 0ull;
@@ -178,7 +182,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       const_cast<IdT *>(t_dst)[p] = (IdT)__ldg(&T.p_dst[p]);
     }
   }
-  for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) hver[x] = 0u;
+  for (uint32_t x = tid; x < N; x += nthr) hver[x] = 0u;
+  for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) s_peers[x] = 0u;
   for (uint32_t x = d_lo + tid; x <= d_hi; x += nthr) s_inptr[x] = __ldg(&in_ptr[x]);
   for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
   if (worklist)
@@ -188,8 +193,14 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     s_arr[0] = s_arr[1] = 0u;
     s_V = s_D = s_M = 0ull;
   }
-  (void)NW;
-  cluster_barrier();  // peers may read our rows / add to our counters from now on
+  cluster_barrier();  // peers may add to our counters / mirror lists from now on
+  if (Q > 1) {  // register as a mirror of the remote sources of own in-links
+    for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
+      const uint32_t sp = t_src[q];
+      if (sp - d_lo >= d_hi - d_lo) dsmem_or_b32(dsmem_addr(s_peers + sp, owner_of(sp)), 1u << crank);
+    }
+    cluster_barrier();
+  }
 
   unsigned long long t = 0ull, t_prev = 0ull;
   uint32_t e = 0u, E = 0u;
@@ -300,6 +311,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
           hver[d] = e;
           cur[q] = kNone;
+          if (Q > 1) {  // push to the mirrors of d (ordered before the peers' reads by the cluster barrier)
+            for (uint32_t pm = s_peers[d]; pm; pm &= pm - 1u) {
+              const uint32_t r = __ffs(pm) - 1u;
+              if constexpr (ROWS_SMEM) dsmem_or_b32(dsmem_addr(&held[(size_t)d * Wr + (c >> 5)], r), 1u << (c & 31u));
+              dsmem_st_u32(dsmem_addr(&hver[d], r), e);
+            }
+          }
           // a relayed chunk (not in post[d]) is held but not required
           if (!MASKED || ((__ldg(&T.post[(size_t)d * Wp + (c >> 5)]) >> (c & 31u)) & 1u)) ++arr;
         }
@@ -392,7 +410,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         // held[src] row of in-link p into registers (own shared memory, a peer's via DSMEM, or L2)
         auto load_row = [&](uint32_t p, uint4 (&cv)[V]) {
           const uint32_t sp = t_src[p];
-          const bool own_src = Q == 1 || sp - d_lo < d_hi - d_lo;
+          const bool own_src = true;  // shared-memory rows: own or mirrored
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
           if (!ROWS_SMEM) {  // rows in HBM/L2, written by other SMs of the cluster: L2-coherent loads
             const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
@@ -546,6 +564,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           uint32_t ordp = 0;  // slot of rank s in bits [4s, 4s + 4)
 #pragma unroll
           for (int j = 0; j < kRegDeg; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
+          const long long dbg_pro = job.trace != nullptr ? clock64() : 0;  // debug (TACOS_TRACE)
           uint4 nxt[V];
           load_row(b0 + (ordp & 15u), nxt);
           for (uint32_t s = 0; s < nlive; ++s) {
@@ -561,6 +580,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               }
             }
             step_row(p, pick[p], cv);
+          }
+          if (job.trace != nullptr) {
+            atomicMax(&s_dbg[2], (unsigned)(dbg_pro - pm_t0));
+            atomicMax(&s_dbg[3], (unsigned)(clock64() - dbg_pro));
+            atomicMax(&s_dbg[4], nlive);
           }
           if constexpr (!kHaveSmem) {
 #pragma unroll
@@ -619,7 +643,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (int j = 0; j < kRegDeg; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
           auto load_half = [&](uint32_t pp, uint4 (&cv)[V]) {
             const uint32_t sp = t_src[pp];
-            const bool own_src = Q == 1 || sp - d_lo < d_hi - d_lo;
+            const bool own_src = true;  // shared-memory rows: own or mirrored
             if (!ROWS_SMEM) {
               const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
 #pragma unroll
@@ -934,7 +958,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       for (int i = 1; i < 9; ++i) tr[3 + i] = (unsigned long long)(ts[i] - ts[i - 1]);
       tr[12] = s_dbg[0];
       tr[13] = s_dbg[1];
-      s_dbg[0] = s_dbg[1] = 0u;
+      tr[14] = s_dbg[2];
+      tr[15] = s_dbg[3];
+      tr[16] = s_dbg[4];
+      s_dbg[0] = s_dbg[1] = s_dbg[2] = s_dbg[3] = s_dbg[4] = 0u;
     }
     if (tn == ~0ull) {  // nothing in flight and not done: stall (R17)
       status = -3;

@@ -52,7 +52,7 @@ struct Job {
   unsigned long long *trace;  // debug (TACOS_TRACE): per CTA rank, per event {t, delivered, local min, matches}
 };
 constexpr uint32_t kTraceEvents = 4096;
-constexpr uint32_t kTraceWords = 14;  // t, delivered, t_next, matches, 8 phase durations, slowest PM / record thread
+constexpr uint32_t kTraceWords = 17;  // t, delivered, t_next, matches, 8 phase durations, slowest PM / record thread
 
 struct JobOut {
   uint64_t T, V, D, M, E;
@@ -70,7 +70,7 @@ struct Layout {
   uint32_t off_busy, off_cur, off_ord, off_pick, off_seen, off_order, off_lv, off_rch;
   uint32_t off_tsrc, off_tw, off_tlid, off_tdst;  // per-position topology copies (src, w, link id, dst)
   // always in shared memory, after [rows][links] when those are resident
-  uint32_t off_hver, off_bitmap, off_wpre, off_inptr, off_act, off_list;  // bitmap: 2 x ceil(L/32) words (event parity)
+  uint32_t off_hver, off_bitmap, off_wpre, off_inptr, off_act, off_list, off_peers;  // bitmap: 2 x ceil(L/32) words (event parity)
   uint32_t smem_bytes;   // total dynamic smem
   uint32_t rows_in_smem, links_in_smem;
   uint32_t threads;

@@ -63,7 +63,7 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   const uint32_t nbw = (L + 31u) / 32u;
   const uint32_t act_words = (N + 31u) / 32u;
   const uint32_t small = al(N * 4u, 16u) + al(2u * nbw * 4u, 16u) + al(nbw * 4u, 16u) + al((N + 1u) * 4u, 16u) +
-                         al(2u * act_words * 4u, 16u) + al(N * 4u, 16u);
+                         al(2u * act_words * 4u, 16u) + al(N * 4u, 16u) + al(N * 4u, 16u);
   const size_t lim = smem_limit;
   const bool ids16 = N < 65536u && L < 65536u;  // u16 NPU / link ids in the shared-memory link state
   if ((size_t)lay.rows_bytes + lay.links_bytes + small <= lim && ids16) {
@@ -85,6 +85,7 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   lay.off_inptr = s; s += al((N + 1u) * 4u, 16u);
   lay.off_act = s; s += al(2u * act_words * 4u, 16u);
   lay.off_list = s; s += al(N * 4u, 16u);
+  lay.off_peers = s; s += al(N * 4u, 16u);
   lay.smem_bytes = s;
   // threads: enough lanes for every destination row in one pass when possible
   const uint32_t th_max = VPL > 1 ? 512u : 768u;  // matches ThreadsFor<V> (__launch_bounds__)
