@@ -44,6 +44,8 @@ literal_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const La
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_min, s_delivered, s_V, s_D, s_M, s_X;
   __shared__ uint32_t s_nrec;
+  // per-event values with 32-bit shared atomics (64-bit ones are CAS loops on sm_100a)
+  __shared__ uint32_t s_arr, s_min32;
 
   const Job job = jobs[blockIdx.x];
   const DevTopo T = *job.topo;
@@ -87,6 +89,8 @@ literal_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const La
     s_V = s_D = s_M = s_X = 0ull;
     s_nrec = 0u;
     s_min = ~0ull;
+    s_arr = 0u;
+    s_min32 = ~0u;
   }
   __syncthreads();
 
@@ -125,16 +129,16 @@ literal_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const La
         }
       }
       arr = warp_sum_u32(arr);
-      if (lane == 0 && arr) atomicAdd(&s_delivered, (unsigned long long)arr);
+      if (lane == 0 && arr) atomicAdd(&s_arr, arr);
     }
     __syncthreads();
-    if (s_delivered == T.required) {  // done; copies still in flight are outdated
+    if (s_delivered + s_arr == T.required) {  // done; copies still in flight are outdated
       for (uint32_t p = tid; p < L; p += nthr)
         if (cur[p] != kNone) ++myX;
       break;
     }
     ++E;
-    if (tid == 0) s_min = ~0ull;
+    if (tid == 0) s_min32 = ~0u;
 
     // ---- PM: one warp per destination ----
     for (uint32_t d = warp; d < N; d += nwarps) {
@@ -304,17 +308,21 @@ literal_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const La
       __syncwarp();
     }
     __syncthreads();
+    if (tid == 0) {  // every thread has read this event's arrivals
+      s_delivered += s_arr;
+      s_arr = 0u;
+    }
 
-    // ---- PE: next event time ----
+    // ---- PE: next event time (offset from t: in-flight copies end within w < 2^32) ----
     {
       unsigned long long mn = ~0ull;
       for (uint32_t p = tid; p < L; p += nthr)
         if (cur[p] != kNone) mn = busy[p] < mn ? busy[p] : mn;
       mn = warp_min_u64(mn);
-      if (lane == 0 && mn != ~0ull) atomicMin(&s_min, mn);
+      if (lane == 0 && mn != ~0ull) atomicMin(&s_min32, (uint32_t)(mn - t));
     }
     __syncthreads();
-    const unsigned long long tn = s_min;
+    const unsigned long long tn = s_min32 == ~0u ? ~0ull : t + s_min32;
     if (tn == ~0ull) {
       status = -3;
       break;
