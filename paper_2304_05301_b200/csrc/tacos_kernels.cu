@@ -11,6 +11,7 @@
 //
 // Nothing here is shared with the CPU oracle (oracle/): separate sources,
 // separate Philox implementation.
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -87,14 +88,6 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   lay.off_list = s; s += al(N * 4u, 16u);
   lay.off_peers = s; s += al(N * 4u, 16u);
   lay.smem_bytes = s;
-  // threads: enough lanes for every destination row in one pass when possible
-  const uint32_t th_max = VPL > 1 ? 512u : 768u;  // matches ThreadsFor<V> (__launch_bounds__)
-  const uint32_t want = N * P > L / 2 ? N * P : L / 2;
-  uint32_t th = 128;
-  while (th < th_max && th < want) th <<= 1;
-  if (th > th_max) th = th_max;
-  if (th < P) th = P;
-  lay.threads = th;
   // Cluster size: split each job over Q CTAs (SMs) while the grid still fits on
   // the chip and every CTA keeps >= 32 destinations.
   uint32_t Q = 1;
@@ -105,8 +98,21 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   }
   lay.cluster = Q;
   const uint32_t n_own = (N + Q - 1) / Q;
+  // threads: one destination group per own destination in one pass when possible, plus
+  // the warps that write the previous event's records meanwhile (about one thread per 16
+  // own in-links; measured on configs 2, 3, 5)
+  const uint32_t th_max = VPL > 1 ? 512u : 768u;  // matches ThreadsFor<V> (__launch_bounds__)
+  const uint32_t walkers = (n_own * P + 31u) & ~31u;
+  const uint32_t recw = std::max<uint32_t>(64u, ((L / Q) / 16u + 31u) & ~31u);
+  uint32_t th = std::max<uint32_t>(128u, walkers + recw);
+  if (th > th_max) th = th_max;
+  if (th < P) th = P;
+  if (const char *env = getenv("TACOS_THREADS")) {  // tuning override (multiple of 32, <= the kernel bound)
+    const uint32_t want = (uint32_t)atoi(env);
+    if (want >= 64 && want <= th_max && want % 32 == 0 && want >= P) th = want;
+  }
+  lay.threads = th;
   lay.pre_draw = 0u;  // 1: draws made ahead in the previous event's record-offset phase (measured slower)
-  (void)n_own;
   if (const char *env = getenv("TACOS_PRE_DRAW")) lay.pre_draw = (uint32_t)atoi(env);
   return lay;
 }
