@@ -176,6 +176,52 @@ int upload(std::vector<DevBuf> &bufs, int dev, const T *h, size_t n, T **d_out, 
   return TACOS_OK;
 }
 
+// Batched host->device upload: arrays are packed into one pinned staging block and
+// copied with a single cudaMemcpyAsync into one device block (pageable copies of many
+// small arrays each cost a staged, synchronous transfer).
+struct Stager {
+  struct Part {
+    const void *h;
+    size_t off, bytes;
+  };
+  std::vector<Part> parts;
+  size_t total = 0;
+  unsigned char *d_base = nullptr;
+  size_t reserve(size_t bytes) {
+    const size_t off = total;
+    total += (bytes + 255) / 256 * 256;
+    return off;
+  }
+  // the device address of a reserved region (valid after alloc)
+  template <typename T>
+  T *at(size_t off) const {
+    return reinterpret_cast<T *>(d_base + off);
+  }
+  int alloc(std::vector<DevBuf> &bufs, int dev) {
+    DevBuf b;
+    b.dev = dev;
+    b.p = device_pool().alloc(dev, total + 16, &b.cls);
+    if (!b.p) return fail(TACOS_E_NOMEM, "device allocation of %zu bytes failed", total);
+    bufs.push_back(b);
+    d_base = reinterpret_cast<unsigned char *>(b.p);
+    return TACOS_OK;
+  }
+  void put(size_t off, const void *h, size_t bytes) { parts.push_back(Part{h, off, bytes}); }
+  // one pinned staging copy + one H2D copy; synchronizes the stream (the staging block is returned)
+  int copy_sync(int dev, cudaStream_t st) {
+    if (total == 0) return TACOS_OK;
+    size_t cls = 0;
+    void *h = pinned_pool().alloc(dev, total, &cls);
+    if (!h) return fail(TACOS_E_NOMEM, "pinned allocation of %zu bytes failed", total);
+    for (const Part &q : parts) std::memcpy(reinterpret_cast<unsigned char *>(h) + q.off, q.h, q.bytes);
+    cudaError_t e = cudaMemcpyAsync(d_base, h, total, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    pinned_pool().release(dev, h, cls);
+    if (e != cudaSuccess) return fail(TACOS_E_CUDA, "staged upload: %s", cudaGetErrorString(e));
+    return TACOS_OK;
+  }
+};
+
 int dev_alloc(std::vector<DevBuf> &bufs, int dev, size_t n, void **d_out) {
   DevBuf b;
   b.dev = dev;
@@ -252,8 +298,16 @@ extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_
   t->dst.assign(dst, dst + n_links);
   t->alpha.assign(alpha_ns, alpha_ns + n_links);
   t->bw.assign(bw, bw + n_links);
-  std::unordered_map<uint64_t, int32_t> pair_id;
-  pair_id.reserve((size_t)n_links * 2);
+  // (src, dst) -> link id: open addressing, linear probing, load <= 1/2
+  size_t cap = 16;
+  while (cap < (size_t)n_links * 2) cap <<= 1;
+  std::vector<uint64_t> hkey(cap, ~0ull);
+  std::vector<int32_t> hval(cap, -1);
+  auto slot_of = [&](uint64_t key) {
+    size_t h = (size_t)((key * 0x9E3779B97F4A7C15ull) >> 20) & (cap - 1);
+    while (hkey[h] != ~0ull && hkey[h] != key) h = (h + 1) & (cap - 1);
+    return h;
+  };
   for (int32_t l = 0; l < n_links; ++l) {
     const int32_t a = src[l], b = dst[l];
     if (a < 0 || a >= n_npus || b < 0 || b >= n_npus)
@@ -261,13 +315,16 @@ extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_
     if (a == b) return fail(TACOS_E_TOPOLOGY, "link %d: self-loop on NPU %d", l, a);
     if (bw[l] == 0) return fail(TACOS_E_TOPOLOGY, "link %d: bandwidth 0", l);
     const uint64_t key = ((uint64_t)(uint32_t)a << 32) | (uint32_t)b;
-    if (!pair_id.emplace(key, l).second)
-      return fail(TACOS_E_TOPOLOGY, "link %d duplicates link %d (%d -> %d)", l, pair_id[key], a, b);
+    const size_t h = slot_of(key);
+    if (hkey[h] == key) return fail(TACOS_E_TOPOLOGY, "link %d duplicates link %d (%d -> %d)", l, hval[h], a, b);
+    hkey[h] = key;
+    hval[h] = l;
   }
   t->rev.assign(n_links, -1);
   for (int32_t l = 0; l < n_links; ++l) {
-    auto it = pair_id.find(((uint64_t)(uint32_t)dst[l] << 32) | (uint32_t)src[l]);
-    if (it != pair_id.end()) t->rev[l] = it->second;
+    const uint64_t key = ((uint64_t)(uint32_t)dst[l] << 32) | (uint32_t)src[l];
+    const size_t h = slot_of(key);
+    if (hkey[h] == key) t->rev[l] = hval[h];
   }
   // CSR per orientation; within a destination, positions in ascending link id
   for (int o = 0; o < 2; ++o) {
@@ -295,17 +352,34 @@ extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_
   if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) {
     t->device = dev;
     int rc;
+    Stager sg;
+    const size_t lb = (size_t)n_links * 4;
+    size_t o_ptr[2], o_lid[2], o_src[2], o_dst[2];
     for (int o = 0; o < 2; ++o) {
-      if ((rc = upload(t->bufs, dev, t->in_ptr[o].data(), t->in_ptr[o].size(), &t->d_in_ptr[o]))) return rc;
-      if ((rc = upload(t->bufs, dev, t->pos_lid[o].data(), (size_t)n_links, &t->d_pos_lid[o]))) return rc;
-      if ((rc = upload(t->bufs, dev, t->pos_src[o].data(), (size_t)n_links, &t->d_pos_src[o]))) return rc;
-      if ((rc = upload(t->bufs, dev, t->pos_dst[o].data(), (size_t)n_links, &t->d_pos_dst[o]))) return rc;
+      o_ptr[o] = sg.reserve(t->in_ptr[o].size() * 4);
+      o_lid[o] = sg.reserve(lb);
+      o_src[o] = sg.reserve(lb);
+      o_dst[o] = sg.reserve(lb);
     }
-    std::vector<uint32_t> us(src, src + n_links), ud(dst, dst + n_links);
-    if ((rc = upload(t->bufs, dev, us.data(), (size_t)n_links, &t->d_src))) return rc;
-    if ((rc = upload(t->bufs, dev, ud.data(), (size_t)n_links, &t->d_dst))) return rc;
-    if ((rc = upload(t->bufs, dev, t->rev.data(), (size_t)n_links, &t->d_rev))) return rc;
-    CUDA_TRY(cudaStreamSynchronize(nullptr));
+    const size_t o_s = sg.reserve(lb), o_d = sg.reserve(lb), o_r = sg.reserve(lb);
+    if ((rc = sg.alloc(t->bufs, dev))) return rc;
+    for (int o = 0; o < 2; ++o) {
+      sg.put(o_ptr[o], t->in_ptr[o].data(), t->in_ptr[o].size() * 4);
+      sg.put(o_lid[o], t->pos_lid[o].data(), lb);
+      sg.put(o_src[o], t->pos_src[o].data(), lb);
+      sg.put(o_dst[o], t->pos_dst[o].data(), lb);
+      t->d_in_ptr[o] = sg.at<uint32_t>(o_ptr[o]);
+      t->d_pos_lid[o] = sg.at<uint32_t>(o_lid[o]);
+      t->d_pos_src[o] = sg.at<uint32_t>(o_src[o]);
+      t->d_pos_dst[o] = sg.at<uint32_t>(o_dst[o]);
+    }
+    sg.put(o_s, src, lb);  // int32 ids < 2^31: the same bytes as uint32
+    sg.put(o_d, dst, lb);
+    sg.put(o_r, t->rev.data(), lb);
+    t->d_src = sg.at<uint32_t>(o_s);
+    t->d_dst = sg.at<uint32_t>(o_d);
+    t->d_rev = sg.at<int32_t>(o_r);
+    if ((rc = sg.copy_sync(dev, nullptr))) return rc;
   } else {
     cudaGetLastError();
   }
