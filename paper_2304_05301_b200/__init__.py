@@ -18,7 +18,7 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtacos.so")
+LIB_PATH = os.environ.get("TACOS_LIB") or os.path.join(_HERE, "libtacos.so")  # TACOS_LIB: a tuning variant built by build.py --variant
 
 TACOS_OK = 0
 TACOS_E_INVALID_ARG = -1

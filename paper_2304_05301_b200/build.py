@@ -23,13 +23,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """variant: build libtacos_<variant>.so with extra -D defines (tuning experiments, loaded
+    through TACOS_LIB); the default library is libtacos.so."""
+    lib = LIB if not variant else os.path.join(HERE, f"libtacos_{variant}.so")
+    if not variant and not force and not _stale():
         return LIB
-    bdir = os.path.join(HERE, "build")
+    bdir = os.path.join(HERE, "build" if not variant else f"build_{variant}")
     os.makedirs(bdir, exist_ok=True)
     objs = []
-    common = ["-O3", "-std=c++17", "-I", INC, "-I", CSRC, "-Xcompiler", "-fPIC"]
+    common = ["-O3", "-std=c++17", "-I", INC, "-I", CSRC, "-Xcompiler", "-fPIC"] + [f"-D{d}" for d in defines]
     cmds = []
     for src in SOURCES:
         obj = os.path.join(bdir, src + ".o")
@@ -45,14 +48,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
         for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
             f.result()
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs + ["-lpthread", "-ldl", "-lrt"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--variant NAME -DFOO=1 ...]
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else ""
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, variant=var, defines=defs))

@@ -44,10 +44,22 @@ constexpr int kRegDeg = 8;  // in-degree handled in registers by the P == 1 path
 // P == 1 register path: true = `have` row in shared memory (step_row), false = in registers
 // (the lane-pair path with one lane)
 constexpr bool kP1Smem = true;
+#ifndef TACOS_P1_HAVE_REG  // 1: the P == 1 walk keeps have[d] in registers (experiment)
+#define TACOS_P1_HAVE_REG 0
+#endif
 
+#ifndef TACOS_P1_HOIST  // 1: the one-thread walker loads every slot's link state before its draws
+#define TACOS_P1_HOIST 0
+#endif
+#ifndef TACOS_WIDE_PREFETCH  // 1: next-row prefetch in the wide-row register walk (needs registers)
+#define TACOS_WIDE_PREFETCH 0
+#endif
+#ifndef TACOS_V4_THREADS  // thread bound of the 4-vector kernels (registers: 65536 / bound per thread)
+#define TACOS_V4_THREADS 384
+#endif
 template <int V>
 struct ThreadsFor {
-  static constexpr int value = V > 1 ? 512 : 768;  // registers: <= 128 resp. <= 85 per thread
+  static constexpr int value = V > 1 ? TACOS_V4_THREADS : 768;  // registers: <= 128 resp. <= 85 per thread
 };
 
 // MASKED (relays, R22): candidates are also and-ed with the
@@ -58,7 +70,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
   // one thread per destination with shared-memory rows: `have` stays in shared memory and a
   // claim is one word update (no per-word predicated register updates)
-  constexpr bool kHaveSmem = (P == 1) && ROWS_SMEM;
+  constexpr bool kHaveSmem = (P == 1) && ROWS_SMEM && !TACOS_P1_HAVE_REG;
   extern __shared__ __align__(16) unsigned char smem[];
   // 64-bit shared atomics are CAS loops on sm_100a: per-event values use 32-bit atomics
   // (arrivals of one event; next event time as an offset from t, < 2^32 since w < 2^32)
@@ -118,7 +130,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   uint32_t *bitmap2 = reinterpret_cast<uint32_t *>(smem + lay.off_bitmap);  // 2 x nbw words (event parity)
   uint32_t *wpre = reinterpret_cast<uint32_t *>(smem + lay.off_wpre);
   uint32_t *s_inptr = reinterpret_cast<uint32_t *>(smem + lay.off_inptr);  // CSR offsets, own range
-  uint32_t *s_act = reinterpret_cast<uint32_t *>(smem + lay.off_act);      // worklist bitmaps (2 x act_words)
   uint32_t *s_list = reinterpret_cast<uint32_t *>(smem + lay.off_list);    // worklist entries
   __shared__ uint32_t s_nwork;
   __shared__ unsigned s_dbg[5];  // debug (TACOS_TRACE): slowest matching / record thread of an event
@@ -131,7 +142,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t chunkN = (N + Q - 1u) / Q;
   const uint32_t d_lo = min(N, crank * chunkN), d_hi = min(N, d_lo + chunkN);
   const uint32_t p_lo = __ldg(&in_ptr[d_lo]), p_hi = __ldg(&in_ptr[d_hi]);
-  const uint32_t act_words = (d_hi - d_lo + 31u) / 32u;
   const bool worklist = lay.worklist != 0u;
   auto cluster_barrier = [&]() {
     if (Q > 1) cluster.sync();
@@ -186,8 +196,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) s_peers[x] = 0u;
   for (uint32_t x = d_lo + tid; x <= d_hi; x += nthr) s_inptr[x] = __ldg(&in_ptr[x]);
   for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
-  if (worklist)
-    for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;
   if (tid == 0) {
     s_delivered = 0ull;
     s_arr[0] = s_arr[1] = 0u;
@@ -296,27 +304,40 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       s_min32[e & 1u] = ~0u;
       s_mcnt[e & 1u] = 0u;
     }
-    if (worklist)
-      for (uint32_t i = tid; i < 2u * act_words; i += nthr) s_act[i] = 0u;
+    if (worklist && tid == 0) s_nwork = 0u;  // read in PW, after the cluster barrier
     {
       uint32_t arr = 0;
       // one thread per in-link position: the arrival (a shared-memory atomicOr on the
       // destination's held row).  With pre_draw the Philox draws of this event were made
       // at the end of the previous one (draw_ahead); the records of event e-1 are written
       // during PM (write_records), away from the cluster barrier's fence.
-      for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
-        const uint32_t c = cur[q];
-        if (c != kNone && busy[q] == t) {  // R7: held by dst from this instant
-          const uint32_t d = t_dst[q];
+      // kPA positions per pass: their link state is loaded before any arrival is applied
+      // (the DSMEM pushes are asm volatile with memory clobbers, which would otherwise
+      // serialize the loads of the next position behind them)
+      constexpr int kPA = 5;
+      for (uint32_t qb = p_lo + tid; qb < p_hi; qb += nthr * kPA) {
+        uint32_t cq[kPA], dq[kPA], pq[kPA];
+        bool arrq[kPA];
+#pragma unroll
+        for (int u = 0; u < kPA; ++u) {
+          const uint32_t q = qb + (uint32_t)u * nthr;
+          cq[u] = q < p_hi ? cur[q] : kNone;
+          arrq[u] = cq[u] != kNone && busy[q] == t;  // R7: held by dst from this instant
+          dq[u] = arrq[u] ? (uint32_t)t_dst[q] : 0u;
+          pq[u] = (Q > 1 && arrq[u]) ? s_peers[dq[u]] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kPA; ++u) {
+          if (!arrq[u]) continue;
+          const uint32_t q = qb + (uint32_t)u * nthr, c = cq[u], d = dq[u];
           atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
           hver[d] = e;
           cur[q] = kNone;
-          if (Q > 1) {  // push to the mirrors of d (ordered before the peers' reads by the cluster barrier)
-            for (uint32_t pm = s_peers[d]; pm; pm &= pm - 1u) {
-              const uint32_t r = __ffs(pm) - 1u;
-              if constexpr (ROWS_SMEM) dsmem_or_b32(dsmem_addr(&held[(size_t)d * Wr + (c >> 5)], r), 1u << (c & 31u));
-              dsmem_st_u32(dsmem_addr(&hver[d], r), e);
-            }
+          // push to the mirrors of d (ordered before the peers' reads by the cluster barrier)
+          for (uint32_t pm = pq[u]; pm; pm &= pm - 1u) {
+            const uint32_t r = __ffs(pm) - 1u;
+            if constexpr (ROWS_SMEM) dsmem_or_b32(dsmem_addr(&held[(size_t)d * Wr + (c >> 5)], r), 1u << (c & 31u));
+            dsmem_st_u32(dsmem_addr(&hver[d], r), e);
           }
           // a relayed chunk (not in post[d]) is held but not required
           if (!MASKED || ((__ldg(&T.post[(size_t)d * Wp + (c >> 5)]) >> (c & 31u)) & 1u)) ++arr;
@@ -347,42 +368,39 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     // For sparse events (heterogeneous costs free few links per event) the destination
     // phase then visits only the destinations that can match; V and D are counted here.
     uint32_t n_work = d_hi - d_lo;
+    uint32_t mo_w = ~0u;  // min offset (busy - t) of own in-flight links (PW / walkers; else PE scans)
     if (worklist) {
-      uint32_t *act = s_act;                    // bit i: own destination d_lo + i has a live in-link
-      uint32_t *anyf = s_act + act_words;       // bit i: ... has a free in-link
-      uint32_t nfree = 0;
-      for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
-        if (busy[q] > t) continue;
-        ++nfree;
-        const uint32_t i = __ldg(&T.p_dst[q]) - d_lo;
-        atomicOr(&anyf[i >> 5], 1u << (i & 31u));
-        if (seen[q] != hver_of(t_src[q])) atomicOr(&act[i >> 5], 1u << (i & 31u));
+      // one thread per own destination: free and live in-links (busy <= t; source changed since
+      // the last empty visit), the min next-free offset of the busy ones; active destinations are
+      // appended with warp-aggregated atomics (their order does not matter: destinations of one
+      // event are independent and the records are ordered by the link-id bitmap)
+      uint32_t nfree = 0, nd = 0;
+      for (uint32_t i0 = 0; i0 < d_hi - d_lo; i0 += nthr) {
+        const uint32_t i = i0 + tid;
+        bool active = false;
+        if (i < d_hi - d_lo) {
+          const uint32_t d = d_lo + i, b0 = s_inptr[d], b1 = s_inptr[d + 1];
+          uint32_t f = 0;
+          for (uint32_t q = b0; q < b1; ++q) {
+            const unsigned long long bq = busy[q];
+            if (bq <= t) {
+              ++f;
+              active = active || seen[q] != hver_of(t_src[q]);
+            } else {
+              mo_w = (uint32_t)(bq - t) < mo_w ? (uint32_t)(bq - t) : mo_w;
+            }
+          }
+          nfree += f;
+          nd += f ? 1u : 0u;
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, active);
+        uint32_t base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&s_nwork, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (active) s_list[base + __popc(bal & ((1u << lane) - 1u))] = d_lo + i;
       }
       myV += nfree;
-      __syncthreads();
-      if (tid < 32) {  // compact the active destinations (ascending id), count D
-        uint32_t running = 0, nd = 0;
-        for (uint32_t base = 0; base < act_words; base += 32u) {
-          const uint32_t i = base + lane;
-          const uint32_t a = i < act_words ? act[i] : 0u;
-          nd += i < act_words ? __popc(anyf[i]) : 0u;
-          const uint32_t c = __popc(a);
-          uint32_t incl = c;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= (uint32_t)o) incl += y;
-          }
-          uint32_t pos = running + incl - c;
-          for (uint32_t bits = a; bits; bits &= bits - 1u) s_list[pos++] = d_lo + i * 32u + (__ffs(bits) - 1u);
-          running += __shfl_sync(0xFFFFFFFFu, incl, 31);
-        }
-        nd = __reduce_add_sync(0xFFFFFFFFu, nd);
-        if (lane == 0) {
-          s_nwork = running;
-          myD += nd;
-        }
-      }
+      myD += nd;
       __syncthreads();
       n_work = s_nwork;
     }
@@ -393,6 +411,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     const uint32_t pm_thr = min(nthr, (n_work * P + 31u) & ~31u);
     const long long pm_t0 = job.trace != nullptr ? clock64() : 0;  // debug: slowest thread of the phase
     uint32_t my_claims = 0;  // this event's matches of this thread (published with the next time)
+    // one-thread register path: the walker also takes the minimum next-free offset of its in-links
+    // (busy beyond t, or claimed now), so PE needs no second pass over the link state
+    constexpr bool kWalkMin = REG_PATH && P == 1 && kP1Smem;
     if (tid >= pm_thr) {
       write_records(pm_thr, nthr - pm_thr, e, rb_prev, t_prev, true);
       if (job.trace != nullptr) atomicMax(&s_dbg[1], (unsigned)(clock64() - pm_t0));
@@ -484,14 +505,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           if constexpr (kHaveSmem) {
             reinterpret_cast<uint32_t *>(have4)[(uint32_t)vsel * 4u + wi] |= mask;  // one word, dynamic index
           } else {
+            const uint32_t sel = (uint32_t)vsel * 4u + wi;  // flat word index: independent predicated ORs
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-              if (vsel == v) {
-                hv[v].x |= wi == 0u ? mask : 0u;
-                hv[v].y |= wi == 1u ? mask : 0u;
-                hv[v].z |= wi == 2u ? mask : 0u;
-                hv[v].w |= wi == 3u ? mask : 0u;
-              }
+              hv[v].x |= sel == (uint32_t)(4 * v + 0) ? mask : 0u;
+              hv[v].y |= sel == (uint32_t)(4 * v + 1) ? mask : 0u;
+              hv[v].z |= sel == (uint32_t)(4 * v + 2) ? mask : 0u;
+              hv[v].w |= sel == (uint32_t)(4 * v + 3) ? mask : 0u;
             }
           }
           uint32_t chunk = (((uint32_t)vsel * P + gl) * 4u + wi) * 32u + bit;
@@ -499,7 +519,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           if (gl == 0) {
             cur[p] = chunk;
             rch[2u * p + (e & 1u)] = (uint16_t)chunk;
-            busy[p] = t + t_w[p];
+            const uint32_t wp = t_w[p];
+            busy[p] = t + wp;
+            mo_w = wp < mo_w ? wp : mo_w;
             ++myM;
             ++my_claims;
             const uint32_t lid = t_lid[p];
@@ -520,12 +542,57 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           //      next in-link's source row loaded while the current one is matched ----
           unsigned long long key[kRegDeg];
           uint32_t nfree = 0, nlive = 0;
+#if TACOS_P1_HOIST
+          // the link state of every slot is loaded before any draw, so the loads of later
+          // slots do not wait behind the Philox chains of earlier ones
+          uint32_t live = 0;  // bit j: slot j is live
+          {
+            unsigned long long bq[kRegDeg];
+            uint32_t sq[kRegDeg], srq[kRegDeg];
+#pragma unroll
+            for (int j = 0; j < kRegDeg; ++j) {
+              const uint32_t q = b0 + (uint32_t)j;
+              const bool in = (uint32_t)j < deg;
+              bq[j] = in ? busy[q] : ~0ull;
+              sq[j] = in ? seen[q] : 0u;
+              srq[j] = in ? (uint32_t)t_src[q] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < kRegDeg; ++j) {
+              const bool in = (uint32_t)j < deg;
+              const bool isfree = in && bq[j] <= t;
+              if (in && !isfree) mo_w = (uint32_t)(bq[j] - t) < mo_w ? (uint32_t)(bq[j] - t) : mo_w;
+              nfree += isfree ? 1u : 0u;
+              if (isfree && sq[j] != hver_of(srq[j])) live |= 1u << j;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < kRegDeg; ++j) {
+            key[j] = ~0ull;
+            if ((live >> j) & 1u) {
+              const uint32_t q = b0 + (uint32_t)j;
+              uint32_t o;
+              if (pre_draw) {
+                o = ord[q];
+              } else {
+                const uint4 r = philox4x32_10(
+                    make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
+                o = r.x;
+                pick[q] = r.y;
+              }
+              ++nlive;
+              key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
+            }
+          }
+#else
 #pragma unroll
           for (int j = 0; j < kRegDeg; ++j) {
             key[j] = ~0ull;
             if ((uint32_t)j < deg) {
               const uint32_t q = b0 + (uint32_t)j;
-              const bool isfree = busy[q] <= t;
+              const unsigned long long bq = busy[q];
+              const bool isfree = bq <= t;
+              if (!isfree) mo_w = (uint32_t)(bq - t) < mo_w ? (uint32_t)(bq - t) : mo_w;
               const bool islive = isfree && seen[q] != hver_of(t_src[q]);
               nfree += isfree ? 1u : 0u;
               if (islive) {
@@ -543,6 +610,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               }
             }
           }
+#endif
           if (!worklist) {
             myV += nfree;
             myD += nfree ? 1u : 0u;
@@ -566,20 +634,24 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (int j = 0; j < kRegDeg; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
           const long long dbg_pro = job.trace != nullptr ? clock64() : 0;  // debug (TACOS_TRACE)
           uint4 nxt[V];
+          if constexpr (!kHaveSmem) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) hv[v] = have4[v];
+          }
           load_row(b0 + (ordp & 15u), nxt);
+          uint32_t pk_nxt = pick[b0 + (ordp & 15u)];  // the pick draw travels with the row prefetch
           for (uint32_t s = 0; s < nlive; ++s) {
             const uint32_t p = b0 + ((ordp >> (4u * s)) & 15u);
             uint4 cv[V];
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = nxt[v];
-            if (s + 1u < nlive) load_row(b0 + ((ordp >> (4u * s + 4u)) & 15u), nxt);
-            if constexpr (!kHaveSmem) {
-              if (s == 0u) {
-#pragma unroll
-                for (int v = 0; v < V; ++v) hv[v] = have4[v];
-              }
+            const uint32_t pk = pk_nxt;
+            if (s + 1u < nlive) {
+              const uint32_t pn = b0 + ((ordp >> (4u * s + 4u)) & 15u);
+              load_row(pn, nxt);
+              pk_nxt = pick[pn];
             }
-            step_row(p, pick[p], cv);
+            step_row(p, pk, cv);
           }
           if (job.trace != nullptr) {
             atomicMax(&s_dbg[2], (unsigned)(dbg_pro - pm_t0));
@@ -727,7 +799,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               const uint32_t chunk = ((((uint32_t)(gl * V) + (uint32_t)vsel) * 4u + wi) * 32u) + bit;
               cur[pp] = chunk;
               rch[2u * pp + (e & 1u)] = (uint16_t)chunk;
-              busy[pp] = t + t_w[pp];
+              const uint32_t wp = t_w[pp];
+              busy[pp] = t + wp;
+              mo_w = wp < mo_w ? wp : mo_w;
               ++myM;
               ++my_claims;
               const uint32_t lid = t_lid[pp];
@@ -741,6 +815,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           //      group path): the group owns the destination's <= kRegDeg in-links, in-link j
           //      in slot j / P of lane j % P; ranks and the walk order stay in registers ----
           constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
+          // the destination's have row (L2 when the rows live in global memory) is loaded
+          // first, so its latency overlaps the draws and the ranking
+#pragma unroll
+          for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v * P + gl];
           unsigned long long key[SL];
           uint32_t pk[SL];
           uint32_t nfree = 0, nlive = 0;
@@ -804,8 +882,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
 #pragma unroll
           for (int sl = 0; sl < SL; ++sl) rk[sl] = key[sl] != ~0ull ? rk[sl] : 0xFFu;
-#pragma unroll
-          for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v * P + gl];
           // walk order: in-link of rank s (owning lane broadcasts position and pick draw)
           auto link_of_rank = [&](uint32_t s, uint32_t &jj, uint32_t &pp) {
             jj = 0;
@@ -824,11 +900,30 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               pp = __shfl_sync(gmask, pp, src_lane);
             }
           };
+#if TACOS_WIDE_PREFETCH
+          // the next in-link's source row is loaded while the current one is matched
+          uint32_t jj, pp;
+          link_of_rank(0u, jj, pp);
+          uint4 nxt[V];
+          load_row(b0 + jj, nxt);
+          for (uint32_t s = 0; s < nlive; ++s) {
+            const uint32_t pc = b0 + jj, pkc = pp;
+            uint4 cv[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) cv[v] = nxt[v];
+            if (s + 1u < nlive) {
+              link_of_rank(s + 1u, jj, pp);
+              load_row(b0 + jj, nxt);
+            }
+            step_row(pc, pkc, cv);
+          }
+#else
           for (uint32_t s = 0; s < nlive; ++s) {
             uint32_t jj, pp;
             link_of_rank(s, jj, pp);
             step(b0 + jj, pp);
           }
+#endif
 #pragma unroll
           for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v * P + gl] = hv[v];
         } else {
@@ -917,7 +1012,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               if (r != crank) dsmem_or_b32(dsmem_addr(bm + i, r), wbits);
         }
       }
-      uint32_t mo = ~0u;
+      // (with the worklist only the active destinations were walked: full pass)
+      const bool walk_min = kWalkMin || worklist;
+      uint32_t mo = walk_min ? mo_w : ~0u;
+      if (!walk_min)
       for (uint32_t p = p_lo + tid; p < p_hi; p += nthr)
         if (cur[p] != kNone) {
           const uint32_t o = (uint32_t)(busy[p] - t);

@@ -1,0 +1,4 @@
+for i in 1 2; do timeout 120 python tools/time_search.py 3 0 50 2>&1 | tail -1; done
+for c in 2 5; do timeout 120 python tools/time_search.py $c 0 20 2>&1 | tail -1; done
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+QS=2 timeout 300 python tools/trace_phases.py 3
