@@ -48,9 +48,6 @@ constexpr bool kP1Smem = true;
 #define TACOS_P1_HAVE_REG 0
 #endif
 
-#ifndef TACOS_P1_HOIST  // 1: the one-thread walker loads every slot's link state before its draws
-#define TACOS_P1_HOIST 0
-#endif
 #ifndef TACOS_WIDE_PREFETCH  // 1: next-row prefetch in the wide-row register walk (needs registers)
 #define TACOS_WIDE_PREFETCH 0
 #endif
@@ -381,13 +378,36 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         if (i < d_hi - d_lo) {
           const uint32_t d = d_lo + i, b0 = s_inptr[d], b1 = s_inptr[d + 1];
           uint32_t f = 0;
-          for (uint32_t q = b0; q < b1; ++q) {
-            const unsigned long long bq = busy[q];
-            if (bq <= t) {
-              ++f;
-              active = active || seen[q] != hver_of(t_src[q]);
-            } else {
-              mo_w = (uint32_t)(bq - t) < mo_w ? (uint32_t)(bq - t) : mo_w;
+          if constexpr (REG_PATH) {  // in-degree <= kRegDeg: every slot's state loaded up front
+            unsigned long long bq[kRegDeg];
+            uint32_t sq[kRegDeg], srq[kRegDeg];
+#pragma unroll
+            for (int j = 0; j < kRegDeg; ++j) {
+              const uint32_t q = b0 + (uint32_t)j;
+              const bool in = q < b1;
+              bq[j] = in ? busy[q] : ~0ull;
+              sq[j] = in ? seen[q] : 0u;
+              srq[j] = in ? (uint32_t)t_src[q] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < kRegDeg; ++j) {
+              const bool in = b0 + (uint32_t)j < b1;
+              if (in && bq[j] <= t) {
+                ++f;
+                active = active || sq[j] != hver_of(srq[j]);
+              } else if (in) {
+                mo_w = (uint32_t)(bq[j] - t) < mo_w ? (uint32_t)(bq[j] - t) : mo_w;
+              }
+            }
+          } else {
+            for (uint32_t q = b0; q < b1; ++q) {
+              const unsigned long long bq = busy[q];
+              if (bq <= t) {
+                ++f;
+                active = active || seen[q] != hver_of(t_src[q]);
+              } else {
+                mo_w = (uint32_t)(bq - t) < mo_w ? (uint32_t)(bq - t) : mo_w;
+              }
             }
           }
           nfree += f;
@@ -542,7 +562,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           //      next in-link's source row loaded while the current one is matched ----
           unsigned long long key[kRegDeg];
           uint32_t nfree = 0, nlive = 0;
-#if TACOS_P1_HOIST
           // the link state of every slot is loaded before any draw, so the loads of later
           // slots do not wait behind the Philox chains of earlier ones
           uint32_t live = 0;  // bit j: slot j is live
@@ -584,33 +603,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
             }
           }
-#else
-#pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) {
-            key[j] = ~0ull;
-            if ((uint32_t)j < deg) {
-              const uint32_t q = b0 + (uint32_t)j;
-              const unsigned long long bq = busy[q];
-              const bool isfree = bq <= t;
-              if (!isfree) mo_w = (uint32_t)(bq - t) < mo_w ? (uint32_t)(bq - t) : mo_w;
-              const bool islive = isfree && seen[q] != hver_of(t_src[q]);
-              nfree += isfree ? 1u : 0u;
-              if (islive) {
-                uint32_t o;
-                if (pre_draw) {
-                  o = ord[q];
-                } else {
-                  const uint4 r = philox4x32_10(
-                      make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
-                  o = r.x;
-                  pick[q] = r.y;
-                }
-                ++nlive;
-                key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
-              }
-            }
-          }
-#endif
           if (!worklist) {
             myV += nfree;
             myD += nfree ? 1u : 0u;
