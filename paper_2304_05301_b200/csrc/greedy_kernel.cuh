@@ -1038,9 +1038,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     rb_prev = rb;
     rb += m_all;
     if (pre_draw && tn != ~0ull) draw_ahead(tn, tid, nthr);  // (optional) the next event's draws
-    if (tracing && e < kTraceEvents) {
+    if (tracing && e % job.trace_stride == 0u && e / job.trace_stride < kTraceEvents) {
       ts[8] = clock64();
-      unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e) * kTraceWords;
+      unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e / job.trace_stride) * kTraceWords;
       tr[0] = t;
       tr[1] = delivered;
       tr[2] = tn;

@@ -839,6 +839,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         jb.g_rows = nullptr;
         jb.g_links = nullptr;
         jb.trace = nullptr;
+        jb.trace_stride = 1u;
         if (!g.lay.rows_in_smem) {
           jb.g_rows = reinterpret_cast<uint32_t *>(pl->d_rows + rows_off);
           rows_off += g.lay.rows_bytes;
@@ -854,6 +855,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     if ((rc = dev_alloc(bufs, dev, 8ull * kTraceWords * kTraceEvents * 8, &vp))) return rc;
     CUDA_TRY(cudaMemset(vp, 0xFF, 8ull * kTraceWords * kTraceEvents * 8));
     pl->jobs[0].trace = reinterpret_cast<unsigned long long *>(vp);
+    pl->jobs[0].trace_stride = 1u;
+    if (const char *env = getenv("TACOS_TRACE_STRIDE")) pl->jobs[0].trace_stride = std::max(1, atoi(env));
     pl->d_trace = pl->jobs[0].trace;
   }
   if ((rc = upload(bufs, dev, pl->jobs.data(), pl->jobs.size(), &pl->d_jobs))) return rc;

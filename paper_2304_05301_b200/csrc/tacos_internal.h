@@ -50,6 +50,7 @@ struct Job {
   uint32_t *g_rows;      // global rows (held | have) when they do not fit in smem
   unsigned char *g_links;// global per-position arrays when they do not fit in smem
   unsigned long long *trace;  // debug (TACOS_TRACE): per CTA rank, per event {t, delivered, local min, matches}
+  uint32_t trace_stride;      // debug: trace every trace_stride-th event (TACOS_TRACE_STRIDE, default 1)
 };
 constexpr uint32_t kTraceEvents = 4096;
 constexpr uint32_t kTraceWords = 17;  // t, delivered, t_next, matches, 8 phase durations, slowest PM / record thread
