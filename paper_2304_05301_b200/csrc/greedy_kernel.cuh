@@ -48,6 +48,9 @@ constexpr bool kP1Smem = true;
 #define TACOS_P1_HAVE_REG 0
 #endif
 
+#ifndef TACOS_MIN_BLOCKS  // resident CTAs per SM the register budget is sized for
+#define TACOS_MIN_BLOCKS 1
+#endif
 #ifndef TACOS_WIDE_PREFETCH  // 1: next-row prefetch in the wide-row register walk (needs registers)
 #define TACOS_WIDE_PREFETCH 0
 #endif
@@ -62,7 +65,7 @@ struct ThreadsFor {
 // MASKED (relays, R22): candidates are also and-ed with the
 // per-position allow row, and only arrivals of chunks in post[dst] count.
 template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM, bool REG_PATH, bool MASKED>
-__global__ void __launch_bounds__(ThreadsFor<V>::value, 1)
+__global__ void __launch_bounds__(ThreadsFor<V>::value, TACOS_MIN_BLOCKS)
 greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Layout lay) {
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
   // one thread per destination with shared-memory rows: `have` stays in shared memory and a
@@ -1110,6 +1113,9 @@ template <int P, int V, bool R, bool K, bool G, bool M = false>
 int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
   auto fn = greedy_kernel<P, V, R, K, G, M>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.smem_bytes);
+  // all of the unified L1 / shared array as shared memory (the kernels stage their state there;
+  // global row loads bypass L1 with ld.cg), so several CTAs can be resident when they fit
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) {
     snprintf(cuda_error_buffer(), 256, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return -4;

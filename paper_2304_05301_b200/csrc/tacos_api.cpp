@@ -978,8 +978,15 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
     if ((rc = job_matches(job, &M))) return rc;
     const Rec *rec = pt.d_rec + (size_t)job * pt.cap;
     uint32_t nl = 0;
-    if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, pt.symmetric ? t->d_rev : nullptr, T_rs, pt.L,
-                                  d_sends, pl->d_sort, pl->sort_bytes, &nl, st)))
+    // one link cost, symmetric, no relays: the mirror order needs no sort (launch_rs_uniform_emit)
+    const bool uniform = pt.symmetric && !coll_relay(&pl->p) && !pt.w.empty() &&
+                         std::all_of(pt.w.begin(), pt.w.end(), [&](uint32_t x) { return x == pt.w[0]; });
+    if (uniform) {
+      if ((rc = launch_rs_uniform_emit(rec, M, t->d_src, t->d_dst, pt.w[0], t->d_rev, T_rs, pt.L, d_sends, pl->d_sort,
+                                       pl->sort_bytes, &nl, st)))
+        return fail(rc, "%s", cuda_error_string());
+    } else if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, pt.symmetric ? t->d_rev : nullptr, T_rs,
+                                         pt.L, d_sends, pl->d_sort, pl->sort_bytes, &nl, st)))
       return fail(rc, "%s", cuda_error_string());
     pl->last_launches += nl;
     if ((rc = drop_late(d_sends, &M))) return rc;

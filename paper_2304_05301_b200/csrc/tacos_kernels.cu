@@ -91,7 +91,8 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   // Cluster size: split each job over Q CTAs (SMs) while the grid still fits on
   // the chip and every CTA keeps >= 32 destinations.
   uint32_t Q = 1;
-  while (Q < 4 && (uint64_t)n_jobs * Q * 2 <= n_sms && N / (Q * 2) >= 32) Q <<= 1;  // Q = 8 measured slower (barriers)
+  // Q = 8 measured slower (barriers); >= 64 destinations per CTA (config 2: Q = 1 0.283 ms vs Q = 2 0.347 ms)
+  while (Q < 4 && (uint64_t)n_jobs * Q * 2 <= n_sms && N / (Q * 2) >= 64) Q <<= 1;
   if (const char *env = getenv("TACOS_CLUSTER")) {
     const uint32_t want = (uint32_t)atoi(env);
     if (want >= 1 && want <= 8 && (want & (want - 1)) == 0) Q = want;
@@ -498,6 +499,105 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
   ++nl;
   if (launches) *launches += nl;
   return check_launch("rs_emit_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// a8, uniform link cost: when every link costs the same w and G is symmetric (RS = the
+// same-seed mirror on the reverse links, R9), the RS key (T_rs - t_start - w, rev[link])
+// orders the AG events in reverse and, inside an event, by reverse link id.  The AG
+// records are sorted by (t_start, link), so an event is a contiguous segment holding each
+// link at most once: the RS position of record i is (M - end of its segment) + the rank of
+// rev[link_i] among the segment's reverse links (a link-id bitmap prefix).  Same order as
+// the radix sort, without it.
+// ---------------------------------------------------------------------------
+__global__ void seg_starts_kernel(const Rec *__restrict__ rec, uint64_t M, uint32_t *__restrict__ starts,
+                                  unsigned int *__restrict__ n_seg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < M; i += (uint64_t)gridDim.x * blockDim.x)
+    if (i == 0 || rec[i].t_start != rec[i - 1].t_start) starts[atomicAdd(n_seg, 1u)] = (uint32_t)i;
+}
+
+__global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, const uint32_t *__restrict__ starts,
+                                       const unsigned int *__restrict__ n_seg, const uint32_t *__restrict__ src,
+                                       const uint32_t *__restrict__ dst, uint32_t w0, const int32_t *__restrict__ rev,
+                                       uint64_t T_rs, uint32_t L, Send32 *__restrict__ out) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t nbw = (L + 31u) / 32u;
+  uint32_t *bm = sm, *pre = sm + nbw;
+  __shared__ unsigned long long s_end;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  const unsigned int nseg = *n_seg;
+  for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const uint64_t s = starts[sg];
+    const unsigned long long ts = rec[s].t_start;
+    for (uint32_t i = tid; i < nbw; i += blockDim.x) bm[i] = 0u;
+    if (tid == 0) s_end = M;
+    __syncthreads();
+    // segment end: the first record after s with another start time
+    for (uint64_t c = s + 1; c < M; c += blockDim.x) {
+      const uint64_t i = c + tid;
+      if (i < M && rec[i].t_start != ts) atomicMin(&s_end, (unsigned long long)i);
+      if (__syncthreads_or(s_end != M)) break;
+    }
+    const uint64_t e = s_end;
+    for (uint64_t i = s + tid; i < e; i += blockDim.x) {
+      const uint32_t l2 = (uint32_t)rev[rec[i].link];
+      atomicOr(&bm[l2 >> 5], 1u << (l2 & 31u));
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive prefix of the bitmap word counts
+      uint32_t running = 0;
+      for (uint32_t b = 0; b < nbw; b += 32u) {
+        const uint32_t i = b + lane;
+        const uint32_t v = i < nbw ? __popc(bm[i]) : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        if (i < nbw) pre[i] = running + incl - v;
+        running += __shfl_sync(0xFFFFFFFFu, incl, 31);
+      }
+    }
+    __syncthreads();
+    const uint64_t base = M - e;
+    for (uint64_t i = s + tid; i < e; i += blockDim.x) {
+      const Rec r = rec[i];
+      const uint32_t l2 = (uint32_t)rev[r.link];
+      const uint32_t rank = pre[l2 >> 5] + __popc(bm[l2 >> 5] & ((1u << (l2 & 31u)) - 1u));
+      Send32 o;
+      o.chunk = r.chunk;
+      o.link = l2;
+      o.src = src[l2];
+      o.dst = dst[l2];
+      o.t0 = T_rs - (r.t_start + w0);
+      o.t1 = T_rs - r.t_start;
+      out[base + rank] = o;
+    }
+    __syncthreads();
+  }
+}
+
+int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, uint32_t w0,
+                           const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
+                           size_t scratch_bytes, uint32_t *launches, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M == 0) return 0;
+  if (scratch_bytes < M * 4 + 256 || M >= (1ull << 32)) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "rs uniform emit: scratch too small");
+    return -9;
+  }
+  unsigned int *n_seg = reinterpret_cast<unsigned int *>(scratch);
+  uint32_t *starts = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(scratch) + 256);
+  cudaMemsetAsync(n_seg, 0, sizeof(unsigned int), st);
+  seg_starts_kernel<<<grid_for(M, 256), 256, 0, st>>>(rec, M, starts, n_seg);
+  int rc = check_launch("seg_starts_kernel");
+  if (rc) return rc;
+  const uint32_t nbw = (L + 31u) / 32u;
+  rs_uniform_emit_kernel<<<148 * 2, 512, 2u * nbw * 4u, st>>>(rec, M, starts, n_seg, src, dst, w0, rev, T_rs, L,
+                                                             reinterpret_cast<Send32 *>(out_sends));
+  if (launches) *launches += 2;
+  return check_launch("rs_uniform_emit_kernel");
 }
 
 // ---------------------------------------------------------------------------
