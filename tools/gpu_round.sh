@@ -13,4 +13,3 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --clock-control none --import-source on -k regex:greedy -s 3 -c 1 -o gpurun_out/prof_c3_bench -f \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 tail -2 gpurun_out/ncu_full.log
-QS=8 timeout 600 python tools/trace_phases.py 4
