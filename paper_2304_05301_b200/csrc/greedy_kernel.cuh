@@ -34,6 +34,8 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "tacos_device.cuh"
@@ -149,8 +151,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   };
   // owner CTA of NPU x = x / chunkN, by a multiply-high with m = ceil(2^32 / chunkN):
   // exact while x * (m * chunkN - 2^32) < 2^32, i.e. for N < 2^16
+  // (chunkN = 1 would need m = 2^32: the owner is x itself)
   const uint32_t own_magic = (uint32_t)((0xFFFFFFFFull + chunkN) / chunkN);
-  auto owner_of = [&](uint32_t x) -> uint32_t { return N < 65536u ? __umulhi(x, own_magic) : x / chunkN; };
+  auto owner_of = [&](uint32_t x) -> uint32_t {
+    return chunkN == 1u ? x : (N < 65536u ? __umulhi(x, own_magic) : x / chunkN);
+  };
   // Mirrors: a CTA keeps local copies of the held rows (shared-memory layout) and source
   // versions of the peers' NPUs that are sources of its in-links; the owner pushes every
   // arrival to them (DSMEM red.or / st) before the cluster barrier, so the matching phase
@@ -1134,6 +1139,12 @@ int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, Job
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (getenv("TACOS_DEBUG_OCC")) {  // debug: co-resident clusters of this shape
+      int ncl = -1;
+      cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg);
+      fprintf(stderr, "tacos: cluster %u x %u threads, %u B smem: max active clusters %d (jobs %u)\n", Q, lay.threads,
+              lay.smem_bytes, ncl, n_jobs);
+    }
     e = cudaLaunchKernelEx(&cfg, fn, d_jobs, d_outs, lay);
     if (e != cudaSuccess) {
       snprintf(cuda_error_buffer(), 256, "cudaLaunchKernelEx (cluster %u): %s", Q, cudaGetErrorString(e));

@@ -312,3 +312,19 @@ def test_literal_custom_replacement(T):
     sch = T.synthesize(t, "CUSTOM", 1, 1, 8, keep_seed_times=True, pre=pre, post=post, n_chunks=1, literal=True)
     assert sch.result["T"] == 2 and sch.result["cancelled"] == 8
     assert_parity(syn, sch, "CUSTOM")
+
+
+@pytest.mark.parametrize("q", [2, 4, 8])
+@pytest.mark.parametrize("case", ["uni4", "torus4x4", "hetero_mesh8x8", "torus8x8x8_k1"])
+def test_forced_cluster_splits(T, monkeypatch, q, case):
+    """Every cluster size on small and large topologies, including splits with one NPU per CTA
+    (uni ring 4 at Q = 4) and CTAs that own no NPU at all (Q = 8 on 4 NPUs)."""
+    topo, k, coll, seeds = {
+        "uni4": (W.uni_ring(4), 1, "AG", 5),
+        "torus4x4": (W.torus([4, 4]), 2, "AR", 6),
+        "hetero_mesh8x8": (W.mesh2d(8, 8, 200, 100), 3, "AR", 4),
+        "torus8x8x8_k1": (W.torus([8, 8, 8]), 1, "AR", 3),
+    }[case]
+    monkeypatch.setenv("TACOS_CLUSTER", str(q))
+    syn, sch, _ = run_both(T, topo, k, 1 << 20, coll, seeds)
+    assert_parity(syn, sch, coll)
