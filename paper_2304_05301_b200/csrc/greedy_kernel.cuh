@@ -1126,6 +1126,31 @@ int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, Job
     return -4;
   }
   const uint32_t Q = lay.cluster ? lay.cluster : 1u;
+  if (g_occ_query) {  // occupancy query (plan build): co-resident clusters / CTAs, no launch
+    int n = 0;
+    if (Q > 1) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(n_jobs * Q, 1, 1);
+      cfg.blockDim = dim3(lay.threads, 1, 1);
+      cfg.dynamicSmemBytes = lay.smem_bytes;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = Q;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) n = 0;
+    } else {
+      int b = 0, dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, (int)lay.threads, lay.smem_bytes) == cudaSuccess) n = b * sms;
+    }
+    cudaGetLastError();
+    *g_occ_query = n;
+    return 0;
+  }
   if (Q > 1) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(n_jobs * Q, 1, 1);

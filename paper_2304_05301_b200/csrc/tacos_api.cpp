@@ -722,6 +722,29 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     }
     g.lay.worklist = (multi_w && g.lay.reg_path) ? 1u : 0u;  // measured: helps the mesh (config 4), not config 5
     if (const char *env = getenv("TACOS_WORKLIST")) g.lay.worklist = (uint32_t)atoi(env);
+    // Cluster size: the largest Q <= 8 (any size, not only powers of two) with jobs * Q <= #SMs,
+    // >= 64 destinations per CTA, and every job's cluster co-resident on the chip (asked of the
+    // occupancy calculator for the kernel this layout selects: only 15 clusters of 8 fit on a
+    // B200, so config 4's 16 jobs take Q = 6, 579 ms vs 625 ms at Q = 4; waves of clusters
+    // would double the time). TACOS_CLUSTER overrides.
+    if (!(p->flags & TACOS_FLAG_LITERAL) && !getenv("TACOS_CLUSTER")) {
+      const uint32_t jobs = n_jobs - begin;
+      for (uint32_t q = 8; q > g.lay.cluster; --q) {
+        if ((uint64_t)jobs * q > (uint64_t)n_sms || maxN / q < 64u) continue;
+        Layout lq = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, jobs, (uint32_t)n_sms, q);
+        lq.reg_path = g.lay.reg_path;
+        lq.masked = g.lay.masked;
+        lq.worklist = g.lay.worklist;
+        int n_active = 0;
+        g_occ_query = &n_active;
+        launch_greedy(lq, P0, V0, nullptr, jobs, nullptr, nullptr);
+        g_occ_query = nullptr;
+        if ((uint32_t)n_active >= jobs) {
+          g.lay = lq;
+          break;
+        }
+      }
+    }
     g.job_begin = begin;
     g.job_end = n_jobs;
     pl->groups.push_back(g);

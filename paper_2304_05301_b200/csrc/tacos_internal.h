@@ -82,8 +82,12 @@ struct Layout {
   uint32_t masked;       // 1: relays (R22): candidates & allow[p], only required arrivals count
 };
 
+// q_force: cluster size to use (0: the automatic choice; TACOS_CLUSTER overrides both)
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,
-                   uint32_t n_sms);
+                   uint32_t n_sms, uint32_t q_force = 0);
+// When set, launch_greedy writes the number of co-resident clusters (CTAs when Q = 1) of the
+// kernel the layout selects into *g_occ_query and launches nothing.
+extern thread_local int *g_occ_query;
 
 // ---- kernel launch wrappers (tacos_kernels.cu) ----
 int launch_greedy(const Layout &lay, uint32_t P, uint32_t VPL, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, void *stream);

@@ -39,8 +39,10 @@ int check_launch(const char *what) {
 // ---------------------------------------------------------------------------
 // Shared-memory / scratch layout of one search job (see greedy_kernel.cuh).
 // ---------------------------------------------------------------------------
+thread_local int *g_occ_query = nullptr;
+
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,
-                   uint32_t n_sms) {
+                   uint32_t n_sms, uint32_t q_force) {
   auto al = [](uint32_t x, uint32_t a) { return (x + a - 1u) / a * a; };
   Layout lay{};
   // pad the shared-memory row stride by one 16-byte vector when the row is an even
@@ -93,9 +95,10 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   uint32_t Q = 1;
   // Q = 8 measured slower (barriers); >= 64 destinations per CTA (config 2: Q = 1 0.283 ms vs Q = 2 0.347 ms)
   while (Q < 4 && (uint64_t)n_jobs * Q * 2 <= n_sms && N / (Q * 2) >= 64) Q <<= 1;
+  if (q_force) Q = q_force;
   if (const char *env = getenv("TACOS_CLUSTER")) {
     const uint32_t want = (uint32_t)atoi(env);
-    if (want >= 1 && want <= 8 && (want & (want - 1)) == 0) Q = want;
+    if (want >= 1 && want <= 8) Q = want;  // any cluster size up to the portable 8
   }
   lay.cluster = Q;
   const uint32_t n_own = (N + Q - 1) / Q;
