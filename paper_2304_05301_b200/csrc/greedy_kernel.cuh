@@ -53,6 +53,9 @@ constexpr bool kP1Smem = true;
 #ifndef TACOS_MIN_BLOCKS  // resident CTAs per SM the register budget is sized for
 #define TACOS_MIN_BLOCKS 1
 #endif
+#ifndef TACOS_WIDE_HAVE_PF  // 1: prefetch the next destination's have row on the wide-row path (experiment)
+#define TACOS_WIDE_HAVE_PF 0
+#endif
 #ifndef TACOS_WIDE_PREFETCH  // 1: next-row prefetch in the wide-row register walk (needs registers)
 #define TACOS_WIDE_PREFETCH 0
 #endif
@@ -448,6 +451,18 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
+#if TACOS_WIDE_HAVE_PF
+      // wide-row register path: the next destination's have row is loaded while this one is walked
+      uint4 hv_pf[V];
+      if constexpr (REG_PATH && P > 2 && !kHaveSmem) {
+        const uint32_t w0 = tid / P;
+        if (w0 < n_work) {
+          const uint4 *h4 = reinterpret_cast<const uint4 *>(have + (size_t)(worklist ? s_list[w0] : d_lo + w0) * Wr);
+#pragma unroll
+          for (int v = 0; v < V; ++v) hv_pf[v] = h4[v * P + gl];
+        }
+      }
+#endif
       for (uint32_t wi = tid / P; wi < n_work; wi += ngroups) {
         const uint32_t d = worklist ? s_list[wi] : d_lo + wi;
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
@@ -817,8 +832,21 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
           // the destination's have row (L2 when the rows live in global memory) is loaded
           // first, so its latency overlaps the draws and the ranking
+#if TACOS_WIDE_HAVE_PF
+#pragma unroll
+          for (int v = 0; v < V; ++v) hv[v] = hv_pf[v];
+          {
+            const uint32_t wn = wi + ngroups;
+            if (wn < n_work) {
+              const uint4 *h4 = reinterpret_cast<const uint4 *>(have + (size_t)(worklist ? s_list[wn] : d_lo + wn) * Wr);
+#pragma unroll
+              for (int v = 0; v < V; ++v) hv_pf[v] = h4[v * P + gl];
+            }
+          }
+#else
 #pragma unroll
           for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v * P + gl];
+#endif
           unsigned long long key[SL];
           uint32_t pk[SL];
           uint32_t nfree = 0, nlive = 0;
