@@ -53,8 +53,8 @@ constexpr bool kP1Smem = true;
 #ifndef TACOS_MIN_BLOCKS  // resident CTAs per SM the register budget is sized for
 #define TACOS_MIN_BLOCKS 1
 #endif
-#ifndef TACOS_WIDE_HAVE_PF  // 1: prefetch the next destination's have row on the wide-row path (experiment)
-#define TACOS_WIDE_HAVE_PF 0
+#ifndef TACOS_P2_SPLIT_DRAWS  // 1: the two-lane path splits the Philox draws between its lanes
+#define TACOS_P2_SPLIT_DRAWS 1
 #endif
 #ifndef TACOS_WIDE_PREFETCH  // 1: next-row prefetch in the wide-row register walk (needs registers)
 #define TACOS_WIDE_PREFETCH 0
@@ -62,15 +62,17 @@ constexpr bool kP1Smem = true;
 #ifndef TACOS_V4_THREADS  // thread bound of the 4-vector kernels (registers: 65536 / bound per thread)
 #define TACOS_V4_THREADS 384
 #endif
-template <int V>
+// thread bound per kernel shape (registers per thread <= 65536 / bound): one vector per lane 768,
+// two-lane groups of two vectors 640 (one group per destination of a 256-destination CTA plus
+// the record warps), otherwise TACOS_V4_THREADS
+template <int P, int V>
 struct ThreadsFor {
-  static constexpr int value = V > 1 ? TACOS_V4_THREADS : 768;  // registers: <= 128 resp. <= 85 per thread
+  static constexpr int value = V == 1 ? 768 : (P == 2 && V == 2) ? 640 : TACOS_V4_THREADS;
 };
-
 // MASKED (relays, R22): candidates are also and-ed with the
 // per-position allow row, and only arrivals of chunks in post[dst] count.
 template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM, bool REG_PATH, bool MASKED>
-__global__ void __launch_bounds__(ThreadsFor<V>::value, TACOS_MIN_BLOCKS)
+__global__ void __launch_bounds__(ThreadsFor<P, V>::value, TACOS_MIN_BLOCKS)
 greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Layout lay) {
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
   // one thread per destination with shared-memory rows: `have` stays in shared memory and a
@@ -451,18 +453,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
     {
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
-#if TACOS_WIDE_HAVE_PF
-      // wide-row register path: the next destination's have row is loaded while this one is walked
-      uint4 hv_pf[V];
-      if constexpr (REG_PATH && P > 2 && !kHaveSmem) {
-        const uint32_t w0 = tid / P;
-        if (w0 < n_work) {
-          const uint4 *h4 = reinterpret_cast<const uint4 *>(have + (size_t)(worklist ? s_list[w0] : d_lo + w0) * Wr);
-#pragma unroll
-          for (int v = 0; v < V; ++v) hv_pf[v] = h4[v * P + gl];
-        }
-      }
-#endif
       for (uint32_t wi = tid / P; wi < n_work; wi += ngroups) {
         const uint32_t d = worklist ? s_list[wi] : d_lo + wi;
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
@@ -686,6 +676,39 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           //      while the current one is matched ----
           unsigned long long key[kRegDeg];
           uint32_t nfree = 0, nlive = 0;
+#if TACOS_P2_SPLIT_DRAWS
+          if constexpr (P == 2) {
+            // the two lanes split the draws (slot j drawn by lane j & 1) and exchange u_ord
+            uint32_t live = 0, od[kRegDeg];
+#pragma unroll
+            for (int j = 0; j < kRegDeg; ++j) {
+              od[j] = 0u;
+              if ((uint32_t)j < deg) {
+                const uint32_t q = b0 + (uint32_t)j;
+                const bool isfree = busy[q] <= t;
+                const bool islive = isfree && seen[q] != hver_of(t_src[q]);
+                nfree += isfree ? 1u : 0u;
+                if (islive) {
+                  live |= 1u << j;
+                  if (pre_draw) {
+                    od[j] = ord[q];
+                  } else if ((uint32_t)(j & 1) == gl) {
+                    const uint4 r = philox4x32_10(
+                        make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
+                    od[j] = r.x;
+                    pick[q] = r.y;
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < kRegDeg; ++j) {
+              const uint32_t o = pre_draw ? od[j] : __shfl_sync(gmask, od[j], j & 1, P);
+              key[j] = ((live >> j) & 1u) ? (((unsigned long long)t_w[b0 + (uint32_t)j] << 32) | o) : ~0ull;
+            }
+            nlive = __popc(live);
+          } else
+#endif
 #pragma unroll
           for (int j = 0; j < kRegDeg; ++j) {
             key[j] = ~0ull;
@@ -832,21 +855,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           constexpr int SL = (kRegDeg + P - 1) / P;  // slots per lane
           // the destination's have row (L2 when the rows live in global memory) is loaded
           // first, so its latency overlaps the draws and the ranking
-#if TACOS_WIDE_HAVE_PF
-#pragma unroll
-          for (int v = 0; v < V; ++v) hv[v] = hv_pf[v];
-          {
-            const uint32_t wn = wi + ngroups;
-            if (wn < n_work) {
-              const uint4 *h4 = reinterpret_cast<const uint4 *>(have + (size_t)(worklist ? s_list[wn] : d_lo + wn) * Wr);
-#pragma unroll
-              for (int v = 0; v < V; ++v) hv_pf[v] = h4[v * P + gl];
-            }
-          }
-#else
 #pragma unroll
           for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v * P + gl];
-#endif
           unsigned long long key[SL];
           uint32_t pk[SL];
           uint32_t nfree = 0, nlive = 0;
