@@ -513,14 +513,20 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
 // rev[link_i] among the segment's reverse links (a link-id bitmap prefix).  Same order as
 // the radix sort, without it.
 // ---------------------------------------------------------------------------
+// starts: the segment starts (unordered); flags[i] = 1 where a segment starts (i < M), 0 up to
+// the 16-byte padded end, so a CTA finds a segment's end with 16-flag vector loads
 __global__ void seg_starts_kernel(const Rec *__restrict__ rec, uint64_t M, uint32_t *__restrict__ starts,
-                                  unsigned int *__restrict__ n_seg) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < M; i += (uint64_t)gridDim.x * blockDim.x)
-    if (i == 0 || rec[i].t_start != rec[i - 1].t_start) starts[atomicAdd(n_seg, 1u)] = (uint32_t)i;
+                                  unsigned int *__restrict__ n_seg, unsigned char *__restrict__ flags, uint64_t n_flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_flags; i += (uint64_t)gridDim.x * blockDim.x) {
+    const bool b = i < M && (i == 0 || rec[i].t_start != rec[i - 1].t_start);
+    flags[i] = b ? 1 : 0;
+    if (b) starts[atomicAdd(n_seg, 1u)] = (uint32_t)i;
+  }
 }
 
 __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, const uint32_t *__restrict__ starts,
-                                       const unsigned int *__restrict__ n_seg, const uint32_t *__restrict__ src,
+                                       const unsigned int *__restrict__ n_seg, const unsigned char *__restrict__ flags,
+                                       uint64_t n_flags, const uint32_t *__restrict__ src,
                                        const uint32_t *__restrict__ dst, uint32_t w0, const int32_t *__restrict__ rev,
                                        uint64_t T_rs, uint32_t L, Send32 *__restrict__ out) {
   extern __shared__ uint32_t sm[];
@@ -531,14 +537,30 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
   const unsigned int nseg = *n_seg;
   for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
     const uint64_t s = starts[sg];
-    const unsigned long long ts = rec[s].t_start;
     for (uint32_t i = tid; i < nbw; i += blockDim.x) bm[i] = 0u;
     if (tid == 0) s_end = M;
     __syncthreads();
-    // segment end: the first record after s with another start time
-    for (uint64_t c = s + 1; c < M; c += blockDim.x) {
-      const uint64_t i = c + tid;
-      if (i < M && rec[i].t_start != ts) atomicMin(&s_end, (unsigned long long)i);
+    // segment end: the next segment start after s (16 flags per thread and pass)
+    for (uint64_t c = (s + 1) & ~15ull; c < M; c += 16ull * blockDim.x) {
+      const uint64_t i0 = c + 16ull * tid;
+      if (i0 < n_flags) {
+        const uint4 f = *reinterpret_cast<const uint4 *>(flags + i0);
+        const uint32_t wv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t m = wv[k];
+          // drop flags at or before s (the pass starts at the 16-aligned position below s + 1)
+          while (m) {
+            const uint32_t byte = (uint32_t)(__ffs(m) - 1) >> 3;
+            const uint64_t i = i0 + 4u * k + byte;
+            if (i > s && i < M) {
+              atomicMin(&s_end, (unsigned long long)i);
+              break;
+            }
+            m &= ~(0xFFu << (8u * byte));
+          }
+        }
+      }
       if (__syncthreads_or(s_end != M)) break;
     }
     const uint64_t e = s_end;
@@ -586,18 +608,20 @@ int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, cons
                            size_t scratch_bytes, uint32_t *launches, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (M == 0) return 0;
-  if (scratch_bytes < M * 4 + 256 || M >= (1ull << 32)) {
+  if (scratch_bytes < 256 + ((M * 4 + 255) / 256) * 256 + M + 16 || M >= (1ull << 32)) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "rs uniform emit: scratch too small");
     return -9;
   }
   unsigned int *n_seg = reinterpret_cast<unsigned int *>(scratch);
   uint32_t *starts = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(scratch) + 256);
+  const uint64_t n_flags = (M + 15u) & ~15ull;
+  unsigned char *flags = reinterpret_cast<unsigned char *>(scratch) + 256 + ((M * 4 + 255) / 256) * 256;
   cudaMemsetAsync(n_seg, 0, sizeof(unsigned int), st);
-  seg_starts_kernel<<<grid_for(M, 256), 256, 0, st>>>(rec, M, starts, n_seg);
+  seg_starts_kernel<<<grid_for(n_flags, 256), 256, 0, st>>>(rec, M, starts, n_seg, flags, n_flags);
   int rc = check_launch("seg_starts_kernel");
   if (rc) return rc;
   const uint32_t nbw = (L + 31u) / 32u;
-  rs_uniform_emit_kernel<<<148 * 2, 512, 2u * nbw * 4u, st>>>(rec, M, starts, n_seg, src, dst, w0, rev, T_rs, L,
+  rs_uniform_emit_kernel<<<148, 1024, 2u * nbw * 4u, st>>>(rec, M, starts, n_seg, flags, n_flags, src, dst, w0, rev, T_rs, L,
                                                              reinterpret_cast<Send32 *>(out_sends));
   if (launches) *launches += 2;
   return check_launch("rs_uniform_emit_kernel");
