@@ -1,0 +1,97 @@
+"""Property-based cases on random strongly connected digraphs (hypothesis).
+
+CPU part: every schedule the oracle produces on a random graph, with random
+link costs (alpha, bw), chunks per NPU and seed, passes the independent replay
+checker (exactly-once delivery, held at departure
+P:L266-267, link intervals disjoint P:L146, maximality and shorter-link-first
+at every event P:L253) and respects the per-node lower bound.
+
+GPU part: the CUDA path through the C ABI against the oracle on the same random
+instances, bit-exact (schedule, per-seed times, counters), for AG / RS / AR and
+both greedy variants (link-first R1/R4 and paper-literal R21).
+"""
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+import oracle
+import workloads as W
+from verify import ag_sets, check, clean
+
+
+@st.composite
+def instances(draw, max_n=9):
+    n = draw(st.integers(2, max_n))
+    n_links = draw(st.integers(n, n * (n - 1))) if n > 2 else 2
+    gseed = draw(st.integers(0, 2**31 - 1))
+    bws = tuple(draw(st.lists(st.sampled_from([1, 7, 25, 50, 100, 400]), min_size=1, max_size=3)))
+    alphas = tuple(draw(st.lists(st.sampled_from([0, 1, 500, 1500, 20000]), min_size=1, max_size=3)))
+    topo = W.random_strongly_connected(n, n_links, gseed, bws=bws, alphas=alphas)
+    k = draw(st.sampled_from([1, 2, 3, 5, 17]))
+    nbytes = draw(st.sampled_from([1, 4096, 1 << 20, 3 << 20]))
+    seed = draw(st.integers(0, 2**64 - 1))
+    return topo, k, nbytes, seed
+
+
+def _bound(topo, w, k):
+    """Smallest T at which every node's in-links could have carried its C - k
+    missing chunks (in-link l moves at most floor(T / w_l) of them by T)."""
+    C = topo.n_npus * k
+    best = 0
+    for d in range(topo.n_npus):
+        ws = [int(w[l]) for l in range(topo.n_links) if int(topo.dst[l]) == d]
+        lo, hi = 0, (C - k) * max(ws)
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if sum(mid // q for q in ws) >= C - k:
+                hi = mid
+            else:
+                lo = mid + 1
+        best = max(best, lo)
+    return best
+
+
+@settings(max_examples=60, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow])
+@given(instances(), st.booleans())
+def test_oracle_schedules_valid_on_random_graphs(inst, literal):
+    topo, k, nbytes, seed = inst
+    w = oracle.link_costs(topo, nbytes)
+    res = oracle.greedy(topo.n_npus, topo.src, topo.dst, w, topo.n_npus * k, k, seed, literal=literal)
+    rep = check(topo.n_npus, topo.src, topo.dst, w, res.sends, *ag_sets(topo.n_npus, k), greedy=not literal)
+    # literal variant (R21): replaced sends are cancelled, so only the final schedule's validity is checked
+    assert clean(rep), {a: b[:5] for a, b in rep.items() if a != "T"}
+    assert rep["T"] == res.T
+    assert len(res.sends) == topo.n_npus * k * (topo.n_npus - 1) == res.M - res.X
+    assert res.T >= _bound(topo, w, k)
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+
+    assert torch.cuda.is_available()
+    from paper_2304_05301_b200 import build
+
+    build.build()
+    import paper_2304_05301_b200 as T
+
+    T.load_library()
+    return T
+
+
+@pytest.mark.gpu
+@settings(max_examples=150, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow,
+                                                                 HealthCheck.function_scoped_fixture])
+@given(instances(max_n=16), st.sampled_from(["AG", "RS", "AR"]), st.booleans(), st.integers(1, 9))
+def test_gpu_parity_on_random_graphs(T, inst, coll, literal, seeds):
+    from test_gpu_parity import assert_parity, oracle_literal_stats
+
+    topo, k, nbytes, base = inst
+    base %= 2**32
+    syn = oracle.synthesize(topo, k, nbytes, coll, [base + s for s in range(seeds)], literal=literal)
+    t = T.Topology.from_workload_topology(topo)
+    sch = T.synthesize(t, coll, k, nbytes, seeds, base, keep_seed_times=True, literal=literal)
+    assert_parity(syn, sch, coll)
+    if literal:
+        assert sch.result["cancelled"] == oracle_literal_stats(syn)
