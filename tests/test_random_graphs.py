@@ -95,3 +95,52 @@ def test_gpu_parity_on_random_graphs(T, inst, coll, literal, seeds):
     assert_parity(syn, sch, coll)
     if literal:
         assert sch.result["cancelled"] == oracle_literal_stats(syn)
+
+
+@st.composite
+def custom_sets(draw, n):
+    """Random pre/post over C chunks: every chunk has >= 1 holder, post is pre
+    plus random requirers (relays make every such instance reachable, R22)."""
+    C = draw(st.integers(1, 40))
+    pre, post = {}, {}
+    for c in range(C):
+        holders = draw(st.lists(st.integers(0, n - 1), min_size=1, max_size=2, unique=True))
+        need = draw(st.lists(st.integers(0, n - 1), max_size=n, unique=True))
+        for x in holders:
+            pre.setdefault(x, []).append(c)
+        for x in set(holders) | set(need):
+            post.setdefault(x, []).append(c)
+    return C, pre, post
+
+
+@pytest.mark.gpu
+@settings(max_examples=80, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow,
+                                                                                   HealthCheck.function_scoped_fixture])
+@given(instances(max_n=14), st.sampled_from(["BROADCAST", "REDUCE", "SCATTER", "GATHER", "CUSTOM"]),
+       st.integers(1, 6), st.data())
+def test_gpu_rooted_and_relay_parity_on_random_graphs(T, inst, coll, seeds, data):
+    """Row f2 on random graphs: rooted collectives from a random root and random
+    CUSTOM pre/post with relays, GPU vs oracle bit-exact, every schedule accepted
+    by tacos_eval."""
+    from test_gpu_f2 import check as f2_check
+
+    topo, k, nbytes, _ = inst
+    n = topo.n_npus
+    root = data.draw(st.integers(0, n - 1))
+    if coll == "CUSTOM":
+        C, pre_s, post_s = data.draw(custom_sets(n))
+        pre, post = oracle.bits_from_sets(n, C, pre_s), oracle.bits_from_sets(n, C, post_s)
+        try:
+            oracle.synthesize(topo, 1, nbytes, coll, [0], pre=pre, post=post, n_chunks=C, relay=True)
+        except oracle.OracleError as e:
+            # R22 relays only toward the nearest requirer that lacks the chunk, so a
+            # requirer on the way can leave another one unreachable: both sides must stall
+            assert e.code == T.TACOS_E_UNREACHABLE
+            t = T.Topology.from_workload_topology(topo)
+            with pytest.raises(T.TacosError) as g:
+                T.synthesize(t, coll, 1, nbytes, seeds, pre=pre, post=post, n_chunks=C, relay=True)
+            assert g.value.code == T.TACOS_E_UNREACHABLE
+            return
+        f2_check(T, topo, coll, 1, seeds, pre=pre, post=post, n_chunks=C, relay=True, nbytes=nbytes)
+    else:
+        f2_check(T, topo, coll, min(k, 5), seeds, root=root, nbytes=nbytes)
