@@ -18,8 +18,8 @@ loops, written from the paper's definitions:
     2 at timestep 0" although NPU 2 does not require chunk 4) forwards chunks
     through NPUs that do not require them.  The greedy rule allows link s -> d
     to carry chunk c when d requires c, or when d is one hop closer than s to
-    the nearest NPU that requires c and does not hold it at the start (hop
-    distance in G).
+    some NPU that requires c and does not hold it at the start (hop distance
+    in G; R22).
   * Multi-tenant (Table VI): several collectives on one network at
     once = the union of their pre/postconditions over disjoint chunk ranges.
     A Reduce tenant inside such a merged forward search is scheduled as the
@@ -103,8 +103,9 @@ def hop_distance_to(n: int, src: Sequence[int], dst: Sequence[int], targets: Seq
 def relay_allow(n: int, src: Sequence[int], dst: Sequence[int], C: int, pre: np.ndarray,
                 post: np.ndarray) -> np.ndarray:
     """allow[l] = post[dst_l] plus the chunks c that dst_l may relay: dst_l does
-    not require c and is one hop closer than src_l to the nearest NPU that
-    requires c and lacks it at the start (R22).  L x ceil(C/32) u32 words."""
+    not require c and lies on a shortest path from src_l to some NPU that
+    requires c and lacks it at the start, i.e. is one hop closer than src_l to
+    that NPU (R22).  L x ceil(C/32) u32 words."""
     pre = np.asarray(pre, dtype=np.uint32).reshape(n, -1)
     post = np.asarray(post, dtype=np.uint32).reshape(n, -1)
     L = len(src)
@@ -115,11 +116,14 @@ def relay_allow(n: int, src: Sequence[int], dst: Sequence[int], C: int, pre: np.
         req = [x for x in range(n) if _get(post, x, c) and not _get(pre, x, c)]
         if not req:
             continue
-        dist = hop_distance_to(n, src, dst, req)
-        for l in range(L):
-            s, d = int(src[l]), int(dst[l])
-            if not _get(post, d, c) and dist[d] >= 0 and dist[s] == dist[d] + 1:
-                allow[l, c >> 5] |= np.uint32(1 << (c & 31))
+        if all(_get(post, x, c) for x in range(n)):
+            continue  # no NPU can relay c
+        for r in req:
+            dist = hop_distance_to(n, src, dst, [r])
+            for l in range(L):
+                s, d = int(src[l]), int(dst[l])
+                if not _get(post, d, c) and dist[d] >= 0 and dist[s] == dist[d] + 1:
+                    allow[l, c >> 5] |= np.uint32(1 << (c & 31))
     return allow
 
 

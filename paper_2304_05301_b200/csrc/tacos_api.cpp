@@ -508,8 +508,9 @@ int problem_bits(uint32_t N, const tacos_synth_params *p, uint32_t &C, std::vect
 
 // R22 relay masks in the position order of orientation o (0: links as given,
 // 1: reversed): allow[q] = post[d] plus the chunks c that d may relay, i.e. d does
-// not require c and is one hop closer than s to the nearest NPU that requires c
-// and lacks it at the start (hop BFS over the oriented links).  Wp words per row.
+// not require c and is one hop closer than s to some NPU r that requires c and
+// lacks it at the start (one hop BFS per such r over the oriented links; chunks
+// every NPU requires have no relays).  Wp words per row.
 void relay_allow(const tacos_topology *t, int o, uint32_t C, uint32_t Wp, const std::vector<uint32_t> &pre,
                  const std::vector<uint32_t> &post, std::vector<uint32_t> &allow) {
   const uint32_t N = (uint32_t)t->N, L = (uint32_t)t->L, W0 = (C + 31u) / 32u;
@@ -522,21 +523,21 @@ void relay_allow(const tacos_topology *t, int o, uint32_t C, uint32_t Wp, const 
   allow.assign((size_t)L * Wp, 0u);
   for (uint32_t q = 0; q < L; ++q)
     for (uint32_t i = 0; i < W0; ++i) allow[(size_t)q * Wp + i] = post[(size_t)pd[q] * W0 + i];
-  std::vector<uint32_t> req, prev_req;
+  std::vector<uint32_t> req;
   std::vector<int32_t> dist(N, -1);
   std::vector<uint32_t> queue;
   for (uint32_t ch = 0; ch < C; ++ch) {
     req.clear();
-    for (uint32_t x = 0; x < N; ++x)
+    bool relayable = false;
+    for (uint32_t x = 0; x < N; ++x) {
       if (bit(post, x, ch) && !bit(pre, x, ch)) req.push_back(x);
-    if (req.empty()) continue;
-    if (req != prev_req) {  // multi-source BFS backwards along in-links
+      if (!bit(post, x, ch)) relayable = true;
+    }
+    if (req.empty() || !relayable) continue;
+    for (uint32_t r : req) {  // BFS backwards along in-links from r
       std::fill(dist.begin(), dist.end(), -1);
-      queue.clear();
-      for (uint32_t x : req) {
-        dist[x] = 0;
-        queue.push_back(x);
-      }
+      queue.assign(1, r);
+      dist[r] = 0;
       for (size_t h = 0; h < queue.size(); ++h) {
         const uint32_t y = queue[h];
         for (uint32_t q = ptr[y]; q < ptr[y + 1]; ++q) {
@@ -547,12 +548,11 @@ void relay_allow(const tacos_topology *t, int o, uint32_t C, uint32_t Wp, const 
           }
         }
       }
-      prev_req = req;
-    }
-    for (uint32_t q = 0; q < L; ++q) {
-      const uint32_t s = ps[q], d = pd[q];
-      if (!bit(post, d, ch) && dist[d] >= 0 && dist[s] == dist[d] + 1)
-        allow[(size_t)q * Wp + (ch >> 5)] |= 1u << (ch & 31u);
+      for (uint32_t q = 0; q < L; ++q) {
+        const uint32_t s = ps[q], d = pd[q];
+        if (!bit(post, d, ch) && dist[d] >= 0 && dist[s] == dist[d] + 1)
+          allow[(size_t)q * Wp + (ch >> 5)] |= 1u << (ch & 31u);
+      }
     }
   }
 }
