@@ -153,3 +153,27 @@ def test_gpu_rooted_and_relay_parity_on_random_graphs(T, inst, coll, seeds, data
         f2_check(T, topo, coll, 1, seeds, pre=pre, post=post, n_chunks=C, relay=True, nbytes=nbytes)
     else:
         f2_check(T, topo, coll, min(k, 5), seeds, root=root, nbytes=nbytes)
+
+
+@pytest.mark.gpu
+@settings(max_examples=40, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow,
+                                                                                   HealthCheck.function_scoped_fixture])
+@given(instances(max_n=10), st.integers(1, 4), st.data())
+def test_gpu_multi_tenant_parity_on_random_graphs(T, inst, seeds, data):
+    """R23 on random graphs: 1-3 concurrent tenants (AG / Broadcast / Scatter /
+    Gather / Reduce, random roots, 1-2 chunks each) merged into one CUSTOM
+    pre/post with relays; GPU vs oracle bit-exact, accepted by tacos_eval, and
+    the merge itself equals oracle.collectives.multi_tenant."""
+    import oracle.collectives as OC
+    from test_gpu_f2 import check as f2_check
+
+    topo, _, nbytes, _ = inst
+    n = topo.n_npus
+    tenants = data.draw(st.lists(st.tuples(st.sampled_from(["AG", "BROADCAST", "SCATTER", "GATHER", "REDUCE"]),
+                                           st.integers(0, n - 1), st.integers(1, 2)), min_size=1, max_size=3))
+    C, pre, post, first = T.multi_tenant(n, tenants)
+    C_o, pre_o, post_o, first_o = OC.multi_tenant(n, tenants)
+    assert (C, list(first)) == (C_o, list(first_o))
+    assert np.array_equal(np.asarray(pre, np.uint32).ravel(), np.asarray(pre_o, np.uint32).ravel())
+    assert np.array_equal(np.asarray(post, np.uint32).ravel(), np.asarray(post_o, np.uint32).ravel())
+    f2_check(T, topo, "CUSTOM", 1, seeds, pre=pre, post=post, n_chunks=C, relay=True, nbytes=nbytes)
