@@ -177,3 +177,32 @@ def test_gpu_multi_tenant_parity_on_random_graphs(T, inst, seeds, data):
     assert np.array_equal(np.asarray(pre, np.uint32).ravel(), np.asarray(pre_o, np.uint32).ravel())
     assert np.array_equal(np.asarray(post, np.uint32).ravel(), np.asarray(post_o, np.uint32).ravel())
     f2_check(T, topo, "CUSTOM", 1, seeds, pre=pre, post=post, n_chunks=C, relay=True, nbytes=nbytes)
+
+
+@settings(max_examples=40, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow])
+@given(instances(max_n=8), st.integers(1, 4))
+def test_oracle_inversion_on_random_graphs(inst, seeds):
+    """P12 on random graphs (symmetric or not): the AR splits into an RS half
+    ending at T_RS and an AG half starting there; the RS half mirrored back
+    (c, b->a, T-t1, T-t0) replays as a valid All-Gather on G^T, mirroring twice
+    is the identity, and the AG half shifted to 0 is a valid greedy All-Gather."""
+    topo, k, nbytes, seed = inst
+    n = topo.n_npus
+    syn = oracle.synthesize(topo, k, nbytes, "AR", [(seed + s) % 2**64 for s in range(seeds)])
+    w = oracle.link_costs(topo, nbytes)
+    rs = syn.sends[syn.sends["t_end"] <= syn.T_rs]
+    ag = syn.sends[syn.sends["t_start"] >= syn.T_rs]
+    assert len(rs) + len(ag) == len(syn.sends) == 2 * n * k * (n - 1)
+    assert syn.T == syn.T_rs + syn.T_ag
+    back = oracle.mirror(rs, syn.T_rs, topo.src, topo.dst, None)
+    gt = W.transpose(topo)
+    rep = check(n, gt.src, gt.dst, w, back, *ag_sets(n, k), greedy=False)
+    assert clean(rep), {a: b[:5] for a, b in rep.items() if a != "T"}
+    assert rep["T"] == syn.T_rs
+    twice = oracle.mirror(back, syn.T_rs, gt.src, gt.dst, None)
+    assert np.array_equal(oracle.canonical(twice), oracle.canonical(rs))
+    ag0 = ag.copy()
+    ag0["t_start"] -= np.uint64(syn.T_rs)
+    ag0["t_end"] -= np.uint64(syn.T_rs)
+    rep2 = check(n, topo.src, topo.dst, w, ag0, *ag_sets(n, k))
+    assert clean(rep2), {a: b[:5] for a, b in rep2.items() if a != "T"}
