@@ -230,7 +230,7 @@ class Synthesis:
     rs_seed: int  # winning RS seed (== seed when G symmetric)
     T_ag: int
     T_rs: int
-    seed_times: np.ndarray  # per seed collective time (AR: T_AR(s) when symmetric)
+    seed_times: np.ndarray  # per seed collective time: AG T_AG(s), RS T_RS(s), AR T_RS(s) + T_AG(s)
     ag: List[GreedyResult]
     rs: List[GreedyResult]
 
@@ -277,8 +277,10 @@ def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "A
     rs_on_gt = need_rs and rev is None
     allow0 = _coll.relay_allow(n, src, dst, C, pre, post) if relay else None
     allow1 = _coll.relay_allow(n, dst, src, C, pre, post) if relay and rs_on_gt else None
-    # the forward runs (sigma 0) are made even when only the G^T phase is used, as by the library
-    jobs_ag = [(s, 0, src, dst, allow0) for s in seeds]
+    # searched jobs: the forward AG on G (sigma 0) unless only the G^T phase is used
+    # (RS / REDUCE / GATHER on an asymmetric graph), and the AG on G^T (sigma 1) for the
+    # RS phase of an asymmetric graph (R9).  V / D / M / E are summed over these jobs.
+    jobs_ag = [] if (only_rs and rs_on_gt) else [(s, 0, src, dst, allow0) for s in seeds]
     jobs_rs = [(s, 1, dst, src, allow1) for s in seeds] if rs_on_gt else []
     with ThreadPoolExecutor(max_workers=threads) as ex:
         res = list(ex.map(run, jobs_ag + jobs_rs))
@@ -286,7 +288,7 @@ def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "A
     rs = res[len(jobs_ag):] if jobs_rs else ag
     T_ag = np.array([r.T for r in ag], dtype=np.uint64)
     T_rs = np.array([r.T for r in rs], dtype=np.uint64)
-    i_ag = int(np.argmin(T_ag))  # argmin returns the first (lowest index) minimum
+    i_ag = int(np.argmin(T_ag)) if len(ag) else 0  # argmin returns the first (lowest index) minimum
     if not need_rs:  # AG, CUSTOM, BROADCAST, SCATTER
         win = ag[i_ag]
         return Synthesis(collective, win.T, canonical(win.sends) if record else win.sends, seeds[i_ag], seeds[i_ag],
@@ -296,8 +298,10 @@ def synthesize(topo, chunks_per_npu: int, chunk_bytes: int, collective: str = "A
         t_ar = T_ag * np.uint64(2) if collective == "AR" else T_ag
         i_ag = i_rs = int(np.argmin(t_ar))
     else:
+        # asymmetric: the RS and AG winners are chosen independently (T_AR = min T_RS + min T_AG);
+        # the per-seed collective time is T_RS(s) + T_AG(s)
         i_rs = int(np.argmin(T_rs))
-        t_ar = (T_rs[i_rs] + T_ag) if collective == "AR" else T_rs
+        t_ar = (T_rs + T_ag) if collective == "AR" else T_rs
     win_rs = rs[i_rs]
     T_RS = win_rs.T
     rs_sends = mirror(win_rs.sends, T_RS, src, dst, rev) if record else win_rs.sends[:0]

@@ -464,20 +464,14 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         // held[src] row of in-link p into registers (own shared memory, a peer's via DSMEM, or L2)
         auto load_row = [&](uint32_t p, uint4 (&cv)[V]) {
           const uint32_t sp = t_src[p];
-          const bool own_src = true;  // shared-memory rows: own or mirrored
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
+          const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
           if (!ROWS_SMEM) {  // rows in HBM/L2, written by other SMs of the cluster: L2-coherent loads
-            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = __ldcg(&h4[v * P + gl]);
-          } else if (own_src) {
-            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
+          } else {  // shared-memory rows: own, or a peer's mirrored copy (pushed in PA)
 #pragma unroll
             for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
-          } else {  // source row in a peer CTA's shared memory (DSMEM)
-            const uint32_t a = dsmem_addr(held + (size_t)sp * Wr, owner_of(sp));
-#pragma unroll
-            for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(v * P + gl) * 16u);
           }
         };
         // One step of the matching walk (a5) on in-link p, pick draw pk, loaded row cv.
@@ -753,19 +747,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (int j = 0; j < kRegDeg; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
           auto load_half = [&](uint32_t pp, uint4 (&cv)[V]) {
             const uint32_t sp = t_src[pp];
-            const bool own_src = true;  // shared-memory rows: own or mirrored
+            const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
             if (!ROWS_SMEM) {
-              const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
 #pragma unroll
               for (int v = 0; v < V; ++v) cv[v] = __ldcg(&h4[gl * V + v]);
-            } else if (own_src) {
-              const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
+            } else {  // own or mirrored row
 #pragma unroll
               for (int v = 0; v < V; ++v) cv[v] = h4[gl * V + v];
-            } else {
-              const uint32_t a = dsmem_addr(held + (size_t)sp * Wr, owner_of(sp));
-#pragma unroll
-              for (int v = 0; v < V; ++v) cv[v] = dsmem_ld4(a + (uint32_t)(gl * V + v) * 16u);
             }
           };
           uint4 hl[V];

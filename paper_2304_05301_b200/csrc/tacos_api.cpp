@@ -159,6 +159,16 @@ struct tacos_topology {
   int32_t *d_rev = nullptr;
   std::vector<DevBuf> bufs;
   ~tacos_topology() {
+    // the blocks go back to a caching pool (no implicit synchronization as with cudaFree):
+    // wait for every kernel that may still read them (a plan built from this topology)
+    if (!bufs.empty()) {
+      int cur = -1;
+      if (cudaGetDevice(&cur) == cudaSuccess && cudaSetDevice(device) == cudaSuccess) {
+        cudaDeviceSynchronize();
+        cudaSetDevice(cur);
+      }
+      cudaGetLastError();
+    }
     for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
   }
 };
@@ -416,6 +426,7 @@ struct Part {
   const tacos_topology *topo = nullptr;
   uint32_t N = 0, L = 0, C = 0, k = 0, Wp = 0, P = 0, VPL = 0;
   bool custom = false, symmetric = false, rs_search = false;
+  uint32_t rs_base = 0;  // first job of the G^T (sigma 1) search: S, or 0 when only the RS phase is searched
   uint64_t required = 0;
   uint64_t cap = 0;  // send records per job (= required without relays)
   std::vector<uint32_t> w;
@@ -453,7 +464,14 @@ struct tacos_plan {
   uint32_t last_launches = 0;
   unsigned long long *d_trace = nullptr;
   unsigned long long *d_count = nullptr;  // compact_sends result (relays)
+  cudaEvent_t done = nullptr;             // recorded after the last search / emit work on its stream
   ~tacos_plan() {
+    // blocks return to the caching pool: wait for the plan's in-flight kernels first
+    if (done) {
+      cudaEventSynchronize(done);
+      cudaEventDestroy(done);
+      cudaGetLastError();
+    }
     for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
     if (h_small_buf.p) pinned_pool().release(h_small_buf.dev, h_small_buf.p, h_small_buf.cls);
   }
@@ -509,11 +527,15 @@ int problem_bits(uint32_t N, const tacos_synth_params *p, uint32_t &C, std::vect
 // R22 relay masks in the position order of orientation o (0: links as given,
 // 1: reversed): allow[q] = post[d] plus the chunks c that d may relay, i.e. d does
 // not require c and is one hop closer than s to some NPU r that requires c and
-// lacks it at the start (one hop BFS per such r over the oriented links; chunks
-// every NPU requires have no relays).  Wp words per row.
+// lacks it at the start (chunks every NPU requires have no relays).  Wp words per row.
+// One backward BFS per distinct requirer r gives the positions on its shortest paths
+// (dist_r[s] = dist_r[d] + 1) as a bitset over positions; a chunk's relay positions are
+// the OR of its requirers' bitsets: O(R (N + L) + C R L / 64) instead of a BFS per
+// (chunk, requirer) pair.
 void relay_allow(const tacos_topology *t, int o, uint32_t C, uint32_t Wp, const std::vector<uint32_t> &pre,
                  const std::vector<uint32_t> &post, std::vector<uint32_t> &allow) {
   const uint32_t N = (uint32_t)t->N, L = (uint32_t)t->L, W0 = (C + 31u) / 32u;
+  const uint32_t LW = (L + 63u) / 64u;  // u64 words of a position bitset
   const auto &ptr = t->in_ptr[o];
   const auto &ps = t->pos_src[o];
   const auto &pd = t->pos_dst[o];
@@ -523,37 +545,61 @@ void relay_allow(const tacos_topology *t, int o, uint32_t C, uint32_t Wp, const 
   allow.assign((size_t)L * Wp, 0u);
   for (uint32_t q = 0; q < L; ++q)
     for (uint32_t i = 0; i < W0; ++i) allow[(size_t)q * Wp + i] = post[(size_t)pd[q] * W0 + i];
-  std::vector<uint32_t> req;
-  std::vector<int32_t> dist(N, -1);
-  std::vector<uint32_t> queue;
+  // chunks with relays: some NPU requires and lacks c, and some NPU does not require c
+  std::vector<std::vector<uint32_t>> req(C);
+  std::vector<char> need_bfs(N, 0);
   for (uint32_t ch = 0; ch < C; ++ch) {
-    req.clear();
     bool relayable = false;
-    for (uint32_t x = 0; x < N; ++x) {
-      if (bit(post, x, ch) && !bit(pre, x, ch)) req.push_back(x);
-      if (!bit(post, x, ch)) relayable = true;
-    }
-    if (req.empty() || !relayable) continue;
-    for (uint32_t r : req) {  // BFS backwards along in-links from r
-      std::fill(dist.begin(), dist.end(), -1);
-      queue.assign(1, r);
-      dist[r] = 0;
-      for (size_t h = 0; h < queue.size(); ++h) {
-        const uint32_t y = queue[h];
-        for (uint32_t q = ptr[y]; q < ptr[y + 1]; ++q) {
-          const uint32_t x = ps[q];
-          if (dist[x] < 0) {
-            dist[x] = dist[y] + 1;
-            queue.push_back(x);
-          }
+    for (uint32_t x = 0; x < N && !relayable; ++x) relayable = !bit(post, x, ch);
+    if (!relayable) continue;
+    for (uint32_t x = 0; x < N; ++x)
+      if (bit(post, x, ch) && !bit(pre, x, ch)) {
+        req[ch].push_back(x);
+        need_bfs[x] = 1;
+      }
+  }
+  // per requirer: positions on its shortest paths (BFS backwards along in-links from r)
+  std::vector<uint32_t> slot(N, ~0u);
+  std::vector<uint64_t> onpath;
+  std::vector<int32_t> dist(N);
+  std::vector<uint32_t> queue;
+  uint32_t n_req = 0;
+  for (uint32_t r = 0; r < N; ++r) {
+    if (!need_bfs[r]) continue;
+    slot[r] = n_req++;
+    onpath.resize((size_t)n_req * LW, 0ull);
+    std::fill(dist.begin(), dist.end(), -1);
+    queue.assign(1, r);
+    dist[r] = 0;
+    for (size_t h = 0; h < queue.size(); ++h) {
+      const uint32_t y = queue[h];
+      for (uint32_t q = ptr[y]; q < ptr[y + 1]; ++q) {
+        const uint32_t x = ps[q];
+        if (dist[x] < 0) {
+          dist[x] = dist[y] + 1;
+          queue.push_back(x);
         }
       }
-      for (uint32_t q = 0; q < L; ++q) {
-        const uint32_t s = ps[q], d = pd[q];
-        if (!bit(post, d, ch) && dist[d] >= 0 && dist[s] == dist[d] + 1)
-          allow[(size_t)q * Wp + (ch >> 5)] |= 1u << (ch & 31u);
-      }
     }
+    uint64_t *row = &onpath[(size_t)slot[r] * LW];
+    for (uint32_t q = 0; q < L; ++q) {
+      const int32_t ds = dist[ps[q]], dd = dist[pd[q]];
+      if (dd >= 0 && ds == dd + 1) row[q >> 6] |= 1ull << (q & 63u);
+    }
+  }
+  std::vector<uint64_t> acc(LW);
+  for (uint32_t ch = 0; ch < C; ++ch) {
+    if (req[ch].empty()) continue;
+    std::fill(acc.begin(), acc.end(), 0ull);
+    for (uint32_t r : req[ch]) {
+      const uint64_t *row = &onpath[(size_t)slot[r] * LW];
+      for (uint32_t i = 0; i < LW; ++i) acc[i] |= row[i];
+    }
+    for (uint32_t i = 0; i < LW; ++i)
+      for (uint64_t m = acc[i]; m; m &= m - 1) {
+        const uint32_t q = i * 64u + (uint32_t)__builtin_ctzll(m);
+        if (!bit(post, pd[q], ch)) allow[(size_t)q * Wp + (ch >> 5)] |= 1u << (ch & 31u);
+      }
   }
 }
 
@@ -660,7 +706,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       pt.cap = pt.required;
     }
     pt.job_base = n_jobs;
-    pt.n_jobs = S * (pt.rs_search ? 2u : 1u);
+    // jobs: S forward searches on G (sigma 0) unless only the RS phase is needed and it is
+    // searched on G^T, then S searches on G^T (sigma 1) for an asymmetric RS phase (R9)
+    const bool fwd = !pt.rs_search || coll_need_ag(p->collective);
+    pt.rs_base = fwd ? S : 0u;
+    pt.n_jobs = (fwd ? S : 0u) + (pt.rs_search ? S : 0u);
     n_jobs += pt.n_jobs;
   }
 
@@ -745,6 +795,9 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         }
       }
     }
+    if ((size_t)g.lay.smem_bytes > smem_limit)  // the per-NPU / per-link arrays that always stay on chip
+      return fail(TACOS_E_OVERFLOW, "search state needs %u B of shared memory per CTA (limit %zu)", g.lay.smem_bytes,
+                  smem_limit);
     g.job_begin = begin;
     g.job_end = n_jobs;
     pl->groups.push_back(g);
@@ -851,7 +904,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       Part &pt = pl->parts[i];
       if (pt.job_base < g.job_begin || pt.job_base >= g.job_end) continue;
       for (uint32_t j = 0; j < pt.n_jobs; ++j) {
-        const uint32_t sigma = j >= S ? 1u : 0u;
+        const uint32_t sigma = (pt.rs_search && j >= pt.rs_base) ? 1u : 0u;
         const uint32_t si = j % S;
         Job &jb = pl->jobs[pt.job_base + j];
         jb.topo = pt.d_topo[sigma];
@@ -887,6 +940,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   pl->h_small_buf.p = pinned_pool().alloc(dev, 8 * 8 * (size_t)n_topos, &pl->h_small_buf.cls);
   if (!pl->h_small_buf.p) return fail(TACOS_E_NOMEM, "pinned allocation failed");
   pl->h_small = reinterpret_cast<uint64_t *>(pl->h_small_buf.p);
+  CUDA_TRY(cudaEventCreateWithFlags(&pl->done, cudaEventDisableTiming));
   CUDA_TRY(cudaStreamSynchronize(nullptr));
   *out = pl.release();
   return TACOS_OK;
@@ -904,11 +958,12 @@ int plan_search(tacos_plan *pl, cudaStream_t st) {
   }
   const uint32_t S = pl->p.n_seeds;
   for (auto &pt : pl->parts) {
-    if ((rc = launch_best_keys(pl->d_outs + pt.job_base, S, pl->p.seed_offset, S, pt.rs_search ? 1u : 0u, pt.d_keys,
+    if ((rc = launch_best_keys(pl->d_outs + pt.job_base, S, pl->p.seed_offset, pt.rs_base, pt.rs_search ? 1u : 0u, pt.d_keys,
                                pt.d_stats, pt.d_times_ag, pt.d_times_rs, st)))
       return fail(rc, "%s", cuda_error_string());
     pl->last_launches++;
   }
+  CUDA_TRY(cudaEventRecord(pl->done, st));
   return TACOS_OK;
 }
 
@@ -996,13 +1051,15 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
     return TACOS_OK;
   };
   if (need_rs && rs_local) {
-    const uint32_t job = pt.symmetric ? (uint32_t)(g_rs - off) : S + (uint32_t)(g_rs - off);
+    const uint32_t job = pt.symmetric ? (uint32_t)(g_rs - off) : pt.rs_base + (uint32_t)(g_rs - off);
     uint64_t M;
     if ((rc = job_matches(job, &M))) return rc;
     const Rec *rec = pt.d_rec + (size_t)job * pt.cap;
     uint32_t nl = 0;
     // one link cost, symmetric, no relays: the mirror order needs no sort (launch_rs_uniform_emit)
+    // (its link-id bitmap lives in shared memory: 2 bits per link, at most 200 KB)
     const bool uniform = pt.symmetric && !coll_relay(&pl->p) && !pt.w.empty() &&
+                         (size_t)8 * ((pt.L + 31u) / 32u) <= (size_t)200 * 1024 &&
                          std::all_of(pt.w.begin(), pt.w.end(), [&](uint32_t x) { return x == pt.w[0]; });
     if (uniform) {
       if ((rc = launch_rs_uniform_emit(rec, M, t->d_src, t->d_dst, pt.w[0], t->d_rev, T_rs, pt.L, d_sends, pl->d_sort,
@@ -1091,7 +1148,9 @@ extern "C" int tacos_plan_emit(tacos_plan *pl, tacos_send *d_sends, uint64_t cap
   int rc = plan_read_small(pl, st);
   if (rc) return rc;
   pl->last_launches = 0;
-  return plan_emit_part(pl, 0, d_sends, capacity, result, st);
+  rc = plan_emit_part(pl, 0, d_sends, capacity, result, st);
+  cudaEventRecord(pl->done, st);
+  return rc;
 }
 
 extern "C" int tacos_plan_stats(tacos_plan *pl, tacos_result *result, void *stream) {
@@ -1213,10 +1272,20 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       cudaError_t e = cudaMemcpyAsync(dst[i], d_out, results[i].n_sends * sizeof(tacos_send), cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "D2H of the schedule: %s", cudaGetErrorString(e));
     }
+    // per-seed collective times (tacos_schedule_seed_times): AG-type T_AG(s); RS-type T_RS(s);
+    // AR T_RS(s) + T_AG(s) (R10), where on a symmetric graph T_RS(s) = T_AG(s) (R9)
+    std::vector<uint64_t> t_ag, t_rs;
+    const bool fwd_jobs = !pt.rs_search || pt.rs_base > 0;
     if (rc == TACOS_OK && seed_times) {
-      seed_times[i].resize(p->n_seeds);
-      cudaError_t e = cudaMemcpyAsync(seed_times[i].data(), pt.d_times_ag, 8 * (size_t)p->n_seeds,
-                                      cudaMemcpyDeviceToHost, st);
+      cudaError_t e = cudaSuccess;
+      if (fwd_jobs) {
+        t_ag.resize(p->n_seeds);
+        e = cudaMemcpyAsync(t_ag.data(), pt.d_times_ag, 8 * (size_t)p->n_seeds, cudaMemcpyDeviceToHost, st);
+      }
+      if (e == cudaSuccess && pt.rs_search) {
+        t_rs.resize(p->n_seeds);
+        e = cudaMemcpyAsync(t_rs.data(), pt.d_times_rs, 8 * (size_t)p->n_seeds, cudaMemcpyDeviceToHost, st);
+      }
       if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "D2H of seed times: %s", cudaGetErrorString(e));
     }
     if (rc == TACOS_OK) {
@@ -1225,8 +1294,15 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     }
     if (tmp.p) device_pool().release(tmp.dev, tmp.p, tmp.cls);
     if (rc) return rc;
-    if (seed_times && p->collective == TACOS_ALL_REDUCE && pt.symmetric)
-      for (auto &v : seed_times[i]) v *= 2;  // T_AR(s) = 2 T_AG(s) on a symmetric graph
+    if (seed_times) {
+      const int coll = p->collective;
+      auto &out = seed_times[i];
+      out.resize(p->n_seeds);
+      for (uint32_t s = 0; s < p->n_seeds; ++s) {
+        const uint64_t ta = fwd_jobs ? t_ag[s] : 0, tr = pt.rs_search ? t_rs[s] : ta;
+        out[s] = !coll_need_rs(coll) ? ta : (coll == TACOS_ALL_REDUCE ? tr + ta : tr);
+      }
+    }
   }
   return TACOS_OK;
 }

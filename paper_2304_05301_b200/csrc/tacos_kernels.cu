@@ -621,7 +621,16 @@ int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, cons
   int rc = check_launch("seg_starts_kernel");
   if (rc) return rc;
   const uint32_t nbw = (L + 31u) / 32u;
-  rs_uniform_emit_kernel<<<148, 1024, 2u * nbw * 4u, st>>>(rec, M, starts, n_seg, flags, n_flags, src, dst, w0, rev, T_rs, L,
+  const uint32_t smem = 2u * nbw * 4u;  // link-id bitmap + its prefix
+  if (smem > 48u * 1024u) {
+    const cudaError_t e = cudaFuncSetAttribute(rs_uniform_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      snprintf(g_cuda_err, sizeof(g_cuda_err), "rs_uniform_emit_kernel: %u B of shared memory: %s", smem,
+               cudaGetErrorString(e));
+      return -4;
+    }
+  }
+  rs_uniform_emit_kernel<<<148, 1024, smem, st>>>(rec, M, starts, n_seg, flags, n_flags, src, dst, w0, rev, T_rs, L,
                                                              reinterpret_cast<Send32 *>(out_sends));
   if (launches) *launches += 2;
   return check_launch("rs_uniform_emit_kernel");

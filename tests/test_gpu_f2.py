@@ -43,7 +43,7 @@ def check(T, topo, coll, k, seeds, root=0, pre=None, post=None, n_chunks=0, rela
     assert r["status"] == 0
     assert r["T"] == syn.T, (r["T"], syn.T)
     assert r["seed"] == syn.seed
-    assert np.array_equal(sch.seed_times, np.array([g.T for g in syn.ag], dtype=np.uint64))
+    assert np.array_equal(sch.seed_times, np.asarray(syn.seed_times, dtype=np.uint64))
     assert (r["visits"], r["dest_events"], r["matches"], r["events"]) == stats(syn)
     assert sch.sends.shape == syn.sends.shape
     assert sch.sends.tobytes() == syn.sends.tobytes()

@@ -7,6 +7,7 @@ record (chunk, src, dst, link, t_start, t_end), and the exact counters
 V (free-link visits), D (destination-events), M (matches), E (events).
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -55,11 +56,8 @@ def assert_parity(syn, sch, coll):
         assert r["T_rs"] == syn.T_rs
     if coll != "RS":
         assert r["T_ag"] == syn.T_ag
-    # per-seed times (AG times; AR on symmetric graphs: 2 T_AG)
-    want_times = np.array([g.T for g in syn.ag], dtype=np.uint64)
-    if coll == "AR" and syn.rs is syn.ag:  # symmetric graph: T_AR(s) = 2 T_AG(s)
-        want_times = want_times * np.uint64(2)
-    assert np.array_equal(sch.seed_times, want_times)
+    # per-seed collective times: AG T_AG(s), RS T_RS(s), AR T_RS(s) + T_AG(s) (= 2 T_AG(s) when symmetric)
+    assert np.array_equal(sch.seed_times, np.asarray(syn.seed_times, dtype=np.uint64))
     assert (r["visits"], r["dest_events"], r["matches"], r["events"]) == oracle_stats(syn)
     assert sch.sends.shape == syn.sends.shape
     assert sch.sends.tobytes() == syn.sends.tobytes()
@@ -100,25 +98,75 @@ def test_hetero_mesh_parity(T, shape):
     assert_parity(syn, sch, "AR")
 
 
-def test_config4_full_size(T):
-    """Config 4 at full size (1024 NPUs, C = 8192, 16 seeds, global rows):
-    seed 0 is compared bit-exactly with the oracle (about 2 CPU-minutes);
-    every seed's schedule-level properties: M = C(N-1) matches, T >= the
-    per-node bound, and the winning AR schedule verifies."""
+def _oracle_c4_seed(args):
+    """One config-4 seed on the oracle: its AR schedule (RS mirror + shifted AG, R9/R10)
+    as a digest, its AG schedule digest and its counters (memory freed before returning)."""
+    import hashlib
+
+    topo, s = args
+    syn = oracle.synthesize(topo, 8, 128 << 10, "AR", [s], threads=1)
+    g = syn.ag[0]
+    ag = oracle.canonical(g.sends)
+    return (s, g.T, g.V, g.D, g.M, g.E, hashlib.sha256(memoryview(np.ascontiguousarray(syn.sends))).hexdigest(),
+            hashlib.sha256(memoryview(np.ascontiguousarray(ag))).hexdigest(), syn.T)
+
+
+def test_config4_every_seed_bit_exact(T):
+    """Config 4 at full size (1024 NPUs, C = 8192, 16 seeds, L2-resident global rows) in the
+    bench's launch configuration (one 16-seed plan): for EVERY seed the AR schedule
+    (16.76 M sends; the RS mirror and the AG half, whose bytes are also compared alone),
+    T_AG(s) and the counters V / D / M / E equal the oracle's; then the one-call best-of-16
+    synthesis returns the oracle's winner and its schedule.  Every seed's AR schedule is
+    emitted from the same searched plan by forcing the best keys to that seed (the
+    multi-GPU owner-emission path).  The oracle runs one seed per host thread (~2 CPU-min
+    per seed)."""
+    import hashlib
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
     wl = W.config(4)
+    S, C, N = 16, 8192, 1024
+    try:
+        import psutil
+
+        mem_workers = max(1, int(psutil.virtual_memory().available // (2 << 30)))
+    except ImportError:
+        mem_workers = 4
+    workers = max(1, min(S, os.cpu_count() or 1, mem_workers))
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        ref = sorted(ex.map(_oracle_c4_seed, [(wl.topo, s) for s in range(S)]))
     t = T.Topology.from_workload_topology(wl.topo)
-    sch = T.synthesize(t, "AR", 8, 128 << 10, 16, keep_seed_times=True)
-    r = sch.result
-    C, N = 8192, 1024
-    assert r["matches"] == 16 * C * (N - 1)
-    assert all(int(x) >= 2 * 5_770_000 for x in sch.seed_times)  # 2 x the corner bound
-    rep = T.evaluate(t, sch.sends, "AR", 8, 128 << 10)
-    assert rep["n_violations"] == 0 and rep["T"] == r["T"]
-    one = T.synthesize(t, "AG", 8, 128 << 10, 1, keep_seed_times=True)
-    g = oracle.synthesize(wl.topo, 8, 128 << 10, "AG", [0])
-    assert one.result["T"] == g.T == int(sch.seed_times[0]) // 2
-    assert one.sends.tobytes() == g.sends.tobytes()
-    assert (one.result["visits"], one.result["dest_events"], one.result["events"]) == (g.ag[0].V, g.ag[0].D, g.ag[0].E)
+    plan = T.Plan(t, "AR", 8, 128 << 10, S)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.search(st)
+    stats = plan.stats(st)
+    assert (stats["visits"], stats["dest_events"], stats["matches"], stats["events"]) == (
+        sum(r[2] for r in ref), sum(r[3] for r in ref), sum(r[4] for r in ref), sum(r[5] for r in ref))
+    assert stats["matches"] == S * C * (N - 1)
+    times = torch.as_tensor(T._CudaArray(plan.seed_times_ptr(), (S,), "<i8"), device="cuda").cpu().numpy().view(np.uint64)
+    assert [int(x) for x in times] == [r[1] for r in ref]
+    out = torch.empty(plan.n_sends * 32, dtype=torch.uint8, device="cuda")
+    keys = plan.best_keys_tensor()
+    M = C * (N - 1)
+    for s, T_ag, *_rest in ref:
+        dig_ar, dig_ag, T_ar = _rest[4], _rest[5], _rest[6]
+        key = T.make_key(T_ag, s)
+        keys.copy_(torch.tensor([key, key], dtype=torch.int64))
+        res = plan.emit(out.data_ptr(), plan.n_sends, st)
+        assert res["T"] == T_ar == 2 * T_ag and res["seed"] == s and res["winner_local"] == 3
+        host = out.cpu().numpy()
+        assert hashlib.sha256(memoryview(host)).hexdigest() == dig_ar, f"seed {s}: AR schedule differs"
+        ag = T.sends_from_bytes(host[M * 32:]).copy()
+        ag["t_start"] -= np.uint64(T_ag)
+        ag["t_end"] -= np.uint64(T_ag)
+        assert hashlib.sha256(memoryview(ag)).hexdigest() == dig_ag, f"seed {s}: AG schedule differs"
+    # the one-call best-of-16 synthesis: winner = min T_AR, ties to the lowest seed (R11)
+    win = min(ref, key=lambda r: (r[1], r[0]))
+    sch = T.synthesize(t, "AR", 8, 128 << 10, S, keep_seed_times=True)
+    assert sch.result["T"] == win[8] and sch.result["seed"] == win[0]
+    assert [int(x) for x in sch.seed_times] == [2 * r[1] for r in ref]
+    assert hashlib.sha256(memoryview(np.ascontiguousarray(sch.sends))).hexdigest() == win[6]
 
 
 @pytest.mark.parametrize("seed", [0, 5, 11])

@@ -1,5 +1,5 @@
 """Time the device search (tacos_plan_search) of a config under the current env.
-usage: python tools/time_search.py CONFIG [no_schedule] [reps]"""
+usage: python tools/time_search.py CONFIG [no_schedule] [reps] [seeds]"""
 import os
 import sys
 
@@ -13,6 +13,8 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 nosch = len(sys.argv) > 2 and sys.argv[2] == "1"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 wl = W.config(cfg)
+if len(sys.argv) > 4:
+    wl.n_seeds = int(sys.argv[4])
 torch.cuda.set_device(0)
 t = T.Topology.from_workload_topology(wl.topo)
 pl = T.Plan(t, wl.collective, wl.chunks_per_npu, wl.chunk_bytes, wl.n_seeds, no_schedule=nosch)
