@@ -48,7 +48,7 @@ TACOS_FLAG_LITERAL = 4
 TACOS_FLAG_RELAY = 8
 
 VIOLATIONS = ("no_such_link", "wrong_duration", "link_overlap", "unheld_at_depart", "duplicate_delivery",
-              "post_unmet", "phase_order")
+              "post_unmet", "phase_order", "not_maximal", "not_shorter_first")
 
 SEND_DTYPE = np.dtype(
     [("chunk", "<u4"), ("src", "<u4"), ("dst", "<u4"), ("link", "<u4"), ("t_start", "<u8"), ("t_end", "<u8")]
@@ -110,7 +110,7 @@ DIM_KINDS = {"ring": TACOS_DIM_RING, "fc": TACOS_DIM_FC, "switch": TACOS_DIM_SWI
 
 class tacos_eval_report(ctypes.Structure):
     _fields_ = [("T", ctypes.c_uint64), ("T_rs", ctypes.c_uint64), ("n_violations", ctypes.c_uint64),
-                ("per_kind", ctypes.c_uint64 * 7), ("first_kind", ctypes.c_int32), ("reserved", ctypes.c_uint32),
+                ("per_kind", ctypes.c_uint64 * len(VIOLATIONS)), ("first_kind", ctypes.c_int32), ("reserved", ctypes.c_uint32),
                 ("first_index", ctypes.c_uint64)]
 
 
@@ -433,8 +433,12 @@ def synthesize_into(topo: Topology, params: tacos_synth_params, sends_ptr: int, 
 
 
 def evaluate(topo: Topology, sends: np.ndarray, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20,
-             time_unit_ns=1, pre=None, post=None, n_chunks=0, root=0) -> dict:
-    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1, 0, 0, time_unit_ns, 0, pre, post, n_chunks, root)
+             time_unit_ns=1, pre=None, post=None, n_chunks=0, root=0, literal=False, relay=False) -> dict:
+    """tacos_eval.  literal / relay name the variant that produced the schedule (the
+    greedy-rule checks apply to link-first searches without relays only)."""
+    flags = (TACOS_FLAG_LITERAL if literal else 0) | (TACOS_FLAG_RELAY if relay else 0)
+    p, keep = make_params(collective, chunks_per_npu, chunk_bytes, 1, 0, 0, time_unit_ns, flags, pre, post, n_chunks,
+                          root)
     return tacos_eval(topo.handle, p, sends)
 
 

@@ -1397,10 +1397,94 @@ struct Checker {
   }
 };
 
+// Greedy rules of one AG-like phase (P:L253 maximal matching per
+// event, P:L263-264 shorter-link-first): replay the events t < T (t = 0 and every
+// arrival time) in order; at t, after the arrivals at t (R7), every idle link a->b
+// (no send on it covers t) must have each candidate c in post[b] & held[a] - held[b]
+// - in flight to b claimed for b by a send starting at t, on a link no costlier than
+// itself.  A link is re-examined only when its source gained a chunk since its last
+// idle examination: its candidates then were all claimed (or reported) and every
+// later candidate must be a newer arrival at the source (held and in-flight sets only
+// grow).  Sends with structural violations are excluded (`ok`).
+void check_greedy_rules(const tacos_topology *t, const std::vector<uint32_t> &w, int o,
+                        const std::vector<tacos_send> &s, const std::vector<size_t> &ok, uint32_t C,
+                        const std::vector<uint32_t> &pre, const std::vector<uint32_t> &post, uint32_t W0,
+                        Checker &ck) {
+  const uint32_t N = (uint32_t)t->N, L = (uint32_t)t->L;
+  if (ok.empty()) return;
+  std::vector<size_t> by_start(ok), by_end(ok);
+  std::stable_sort(by_start.begin(), by_start.end(), [&](size_t x, size_t y) { return s[x].t_start < s[y].t_start; });
+  std::stable_sort(by_end.begin(), by_end.end(), [&](size_t x, size_t y) { return s[x].t_end < s[y].t_end; });
+  uint64_t T = 0;
+  for (size_t i : ok) T = std::max<uint64_t>(T, s[i].t_end);
+  std::vector<uint32_t> held(pre), pend((size_t)N * W0, 0u);
+  (void)C;
+  std::vector<uint32_t> ver(N, 1u), seen(L, 0u);  // source version at the link's last idle examination
+  std::vector<uint64_t> busy_until(L, 0ull);      // end of the latest send started on the link
+  std::vector<std::vector<std::pair<uint32_t, uint32_t>>> claims(N);  // per dst at t: (chunk, cost)
+  std::vector<uint32_t> touched;
+  std::vector<char> starting(L, 0);
+  size_t ia = 0, is = 0;
+  uint64_t tcur = 0;
+  for (;;) {
+    // arrivals at tcur (R7): held by dst, no longer in flight
+    while (ia < by_end.size() && s[by_end[ia]].t_end <= tcur) {
+      const tacos_send &e = s[by_end[ia++]];
+      const size_t wd = (size_t)e.dst * W0 + (e.chunk >> 5);
+      const uint32_t m = 1u << (e.chunk & 31u);
+      held[wd] |= m;
+      pend[wd] &= ~m;
+      ++ver[e.dst];
+    }
+    if (tcur >= T) break;
+    // the matching of event tcur: sends starting at tcur
+    const size_t is0 = is;
+    while (is < by_start.size() && s[by_start[is]].t_start == tcur) {
+      const tacos_send &e = s[by_start[is++]];
+      if (claims[e.dst].empty()) touched.push_back(e.dst);
+      claims[e.dst].push_back({e.chunk, w[e.link]});
+      starting[e.link] = 1;
+    }
+    for (uint32_t l = 0; l < L; ++l) {
+      if (starting[l] || busy_until[l] > tcur) continue;  // not idle at tcur
+      const uint32_t a = (uint32_t)(o == 0 ? t->src[l] : t->dst[l]);
+      const uint32_t b = (uint32_t)(o == 0 ? t->dst[l] : t->src[l]);
+      if (seen[l] == ver[a]) continue;  // source unchanged since its last idle examination
+      seen[l] = ver[a];
+      const uint32_t *ha = &held[(size_t)a * W0], *hb = &held[(size_t)b * W0], *pb = &pend[(size_t)b * W0];
+      const uint32_t *qb = &post[(size_t)b * W0];
+      bool bad_max = false, bad_sf = false;
+      for (uint32_t i = 0; i < W0; ++i) {
+        for (uint32_t m = ha[i] & qb[i] & ~hb[i] & ~pb[i]; m; m &= m - 1) {
+          const uint32_t c = i * 32u + (uint32_t)__builtin_ctz(m);
+          const auto &cl = claims[b];
+          auto it = std::find_if(cl.begin(), cl.end(), [&](const std::pair<uint32_t, uint32_t> &x) { return x.first == c; });
+          if (it == cl.end()) bad_max = true;
+          else if (it->second > w[l]) bad_sf = true;
+        }
+      }
+      if (bad_max) ck.add(TACOS_V_NOT_MAXIMAL, l);
+      if (bad_sf) ck.add(TACOS_V_NOT_SHORTER_FIRST, l);
+    }
+    // this event's sends are in flight from now on
+    for (size_t j = is0; j < is; ++j) {
+      const tacos_send &e = s[by_start[j]];
+      pend[(size_t)e.dst * W0 + (e.chunk >> 5)] |= 1u << (e.chunk & 31u);
+      busy_until[e.link] = std::max<uint64_t>(busy_until[e.link], e.t_end);
+      starting[e.link] = 0;
+    }
+    for (uint32_t x : touched) claims[x].clear();
+    touched.clear();
+    // next event: the next arrival time (matching runs only at arrivals, R20)
+    if (ia >= by_end.size()) break;
+    tcur = s[by_end[ia]].t_end;
+  }
+}
+
 // One AG-like phase on orientation o (0: links as given, 1: reversed).
 void check_phase(const tacos_topology *t, const std::vector<uint32_t> &w, int o, const std::vector<tacos_send> &s,
                  const std::vector<uint64_t> &index, uint32_t C, const std::vector<uint32_t> &pre,
-                 const std::vector<uint32_t> &post, uint32_t W0, Checker &ck) {
+                 const std::vector<uint32_t> &post, uint32_t W0, Checker &ck, bool greedy) {
   const uint32_t N = (uint32_t)t->N;
   const uint64_t kNever = ~0ull;
   std::vector<uint64_t> arrive((size_t)N * C, kNever);
@@ -1451,6 +1535,7 @@ void check_phase(const tacos_topology *t, const std::vector<uint32_t> &w, int o,
     for (uint32_t c = 0; c < C; ++c)
       if (((post[(size_t)x * W0 + (c >> 5)] >> (c & 31)) & 1u) && arrive[(size_t)x * C + c] == kNever)
         ck.add(TACOS_V_POST_UNMET, (uint64_t)x * C + c);
+  if (greedy) check_greedy_rules(t, w, o, s, ok, C, pre, post, W0, ck);
 }
 }  // namespace
 
@@ -1483,6 +1568,9 @@ extern "C" int tacos_eval(const tacos_topology *t, const tacos_synth_params *p, 
         }
     }
     Checker ck{out};
+    // the greedy rules hold for link-first searches without relays (R1, R4); the literal
+    // variant (R21) and relay collectives (R22) follow other rules
+    const bool greedy = (p->flags & TACOS_FLAG_LITERAL) == 0 && !coll_relay(p);
     uint64_t T = 0;
     for (uint64_t i = 0; i < n_sends; ++i) T = std::max<uint64_t>(T, sends[i].t_end);
     out->T = T;
@@ -1490,7 +1578,7 @@ extern "C" int tacos_eval(const tacos_topology *t, const tacos_synth_params *p, 
     std::vector<uint64_t> idx(n_sends);
     for (uint64_t i = 0; i < n_sends; ++i) idx[i] = i;
     if (!coll_need_rs(p->collective)) {  // AG, CUSTOM, BROADCAST, SCATTER
-      check_phase(t, w, 0, all, idx, C, pre, post, W0, ck);
+      check_phase(t, w, 0, all, idx, C, pre, post, W0, ck, greedy);
       return TACOS_OK;
     }
     // RS part (all of an RS; the earliest half of an AR): mirror back into an AG on G^T
@@ -1515,7 +1603,7 @@ extern "C" int tacos_eval(const tacos_topology *t, const tacos_synth_params *p, 
       rs[j] = m;
       rs_idx[j] = order[j];
     }
-    check_phase(t, w, 1, rs, rs_idx, C, pre, post, W0, ck);
+    check_phase(t, w, 1, rs, rs_idx, C, pre, post, W0, ck, greedy);
     if (p->collective == TACOS_ALL_REDUCE) {
       for (uint64_t j = n_rs; j < n_sends; ++j) {
         tacos_send e = all[order[j]];
@@ -1528,7 +1616,7 @@ extern "C" int tacos_eval(const tacos_topology *t, const tacos_synth_params *p, 
         ag.push_back(e);
         ag_idx.push_back(order[j]);
       }
-      check_phase(t, w, 0, ag, ag_idx, C, pre, post, W0, ck);
+      check_phase(t, w, 0, ag, ag_idx, C, pre, post, W0, ck, greedy);
     }
     return TACOS_OK;
   } catch (const std::bad_alloc &) {

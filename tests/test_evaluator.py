@@ -110,3 +110,43 @@ def test_evaluator_rejects_invalid(T):
     with pytest.raises(T.TacosError) as e:
         T.evaluate_continuous(t, bad, "AG", 1, MiB)
     assert e.value.code == T.TACOS_E_VERIFY
+
+
+def test_oracle_evaluator_pinned_to_paper_ratios():
+    """oracle/evaluate.py on its own (no library): the paper's printed ratios
+    P:L107 + P:L120 (100 NPUs, alpha = 0.5 us, 100 GB/s, All-Reduce): Direct is
+    12.88x slower than Ring on the 100-NPU (bidirectional) ring, Ring 99x slower
+    than Direct on FullyConnected(100) -- exact rational times, rounded as printed."""
+    ring = W.bi_ring(100)
+    r = OE.evaluate(ring, OE.baseline(ring, "ring", "AR", 1, MiB), "AR", 1, MiB)[0]
+    d = OE.evaluate(ring, OE.baseline(ring, "direct", "AR", 1, MiB), "AR", 1, MiB)[0]
+    assert round(float(d / r), 2) == 12.88
+    fc = W.fully_connected(100)
+    r = OE.evaluate(fc, OE.baseline(fc, "ring", "AR", 1, MiB), "AR", 1, MiB)[0]
+    d = OE.evaluate(fc, OE.baseline(fc, "direct", "AR", 1, MiB), "AR", 1, MiB)[0]
+    assert round(float(r / d), 2) == 99.00
+
+
+def test_oracle_evaluator_closed_forms():
+    """oracle/evaluate.py against closed forms written from P:L104 (a send lasts
+    alpha + n / bw): one send; k sends of one link serialize (k (alpha + n/bw));
+    the Ring baseline on a uni ring of p NPUs: AG (p - 1)(alpha + n/bw), AR twice
+    that with the RS phase ending half way (textbook ring)."""
+    from fractions import Fraction
+
+    per = Fraction(500) + Fraction(MiB, 100)
+    two = W.Topology(2, np.array([0, 1], np.int32), np.array([1, 0], np.int32), np.array([500, 500], np.uint32),
+                     np.array([100, 100], np.uint32))
+    one = np.zeros(1, dtype=oracle.SEND_DTYPE)
+    one[0] = (1, 1, 0, 1, 0, 10986)
+    assert OE.evaluate(two, one, "AG", 1, MiB) == (per, 0)
+    for k in (2, 5):
+        s = np.zeros(k, dtype=oracle.SEND_DTYPE)
+        for j in range(k):
+            s[j] = (j, 0, 1, 0, 0, 10986)
+        assert OE.evaluate(two, s, "AG", k, MiB)[0] == k * per
+    for p in (3, 4, 7):
+        topo = W.uni_ring(p)
+        assert OE.evaluate(topo, OE.baseline(topo, "ring", "AG", 1, MiB), "AG", 1, MiB)[0] == (p - 1) * per
+        T_ar, T_rs = OE.evaluate(topo, OE.baseline(topo, "ring", "AR", 1, MiB), "AR", 1, MiB)
+        assert (T_ar, T_rs) == (2 * (p - 1) * per, (p - 1) * per)

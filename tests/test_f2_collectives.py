@@ -25,6 +25,7 @@ import oracle
 import oracle.collectives as OC
 import workloads as W
 from bruteforce import optimum
+from verify import check, clean
 
 MiB = 1 << 20
 
@@ -143,12 +144,12 @@ def test_relay_invariants_and_verifier(T, case):
         pre = oracle.bits_from_sets(n, C, {0: [0], 5: [1]})
         post = oracle.bits_from_sets(n, C, {0: [0, 1], 5: [0, 1]})
         syn = oracle.synthesize(topo, 1, MiB, "CUSTOM", list(range(4)), pre=pre, post=post, n_chunks=C, relay=True)
-        rep = T.evaluate(t, syn.sends, "CUSTOM", 1, MiB, pre=pre, post=post, n_chunks=C)
+        rep = T.evaluate(t, syn.sends, "CUSTOM", 1, MiB, pre=pre, post=post, n_chunks=C, relay=True)
         assert syn.T == 5 * oracle.link_cost(500, 100, MiB)  # both chunks walk the 5 hops at once
     elif kind == "TENANTS":
         C, pre, post, first = OC.multi_tenant(n, [("BROADCAST", 2, 1), ("REDUCE", 9, 1), ("AG", 0, 1)])
         syn = oracle.synthesize(topo, 1, MiB, "CUSTOM", list(range(4)), pre=pre, post=post, n_chunks=C, relay=True)
-        rep = T.evaluate(t, syn.sends, "CUSTOM", 1, MiB, pre=pre, post=post, n_chunks=C)
+        rep = T.evaluate(t, syn.sends, "CUSTOM", 1, MiB, pre=pre, post=post, n_chunks=C, relay=True)
         C2, pre2, post2, first2 = T.multi_tenant(n, [("BROADCAST", 2, 1), ("REDUCE", 9, 1), ("AG", 0, 1)])
         assert (C2, first2) == (C, first) and np.array_equal(pre2, pre) and np.array_equal(post2, post)
     else:
@@ -156,9 +157,18 @@ def test_relay_invariants_and_verifier(T, case):
         rep = T.evaluate(t, syn.sends, kind, k, MiB, root=root)
         C, pre, post = OC.named_bits(kind if kind == "SCATTER" else OC.dual(kind), n, k, root)
     assert rep["n_violations"] == 0, rep
-    # relay sends: chunk not required at dst, one hop closer to a requester (on the searched orientation)
+    # the independent replay of tests/verify.py (structural rules; relays follow R22, not the
+    # link-first maximality): a GATHER is mirrored back onto G^T, where it is a Scatter
     sends = syn.sends
     fwd = kind != "GATHER"
+    w = oracle.link_costs(topo, MiB)
+    sets = lambda bits: [{c for c in range(C) if (int(bits[x, c >> 5]) >> (c & 31)) & 1} for x in range(n)]
+    if fwd:
+        v = check(n, topo.src, topo.dst, w, sends, sets(pre), sets(post), greedy=False)
+    else:
+        back = oracle.mirror(sends, syn.T, topo.src, topo.dst, None)
+        v = check(n, topo.dst, topo.src, w, back, sets(pre), sets(post), greedy=False)
+    assert clean(v), v
     a, b = (topo.src, topo.dst) if fwd else (topo.dst, topo.src)
     seen = set()
     for e in sends.tolist():

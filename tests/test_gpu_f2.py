@@ -47,7 +47,7 @@ def check(T, topo, coll, k, seeds, root=0, pre=None, post=None, n_chunks=0, rela
     assert (r["visits"], r["dest_events"], r["matches"], r["events"]) == stats(syn)
     assert sch.sends.shape == syn.sends.shape
     assert sch.sends.tobytes() == syn.sends.tobytes()
-    rep = T.evaluate(t, sch.sends, coll, k, nbytes, pre=pre, post=post, n_chunks=n_chunks, root=root)
+    rep = T.evaluate(t, sch.sends, coll, k, nbytes, pre=pre, post=post, n_chunks=n_chunks, root=root, relay=relay)
     assert rep["n_violations"] == 0, rep
     return syn, sch
 

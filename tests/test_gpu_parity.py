@@ -43,6 +43,9 @@ def run_both(T, topo, k, nbytes, coll, seeds, base_seed=0, pre=None, post=None, 
     t = T.Topology.from_workload_topology(topo)
     sch = T.synthesize(t, coll, k, nbytes, seeds, base_seed, keep_seed_times=True, pre=pre, post=post,
                        n_chunks=n_chunks)
+    # every GPU schedule also replays clean through tacos_eval, greedy rules included (P11)
+    rep = T.evaluate(t, sch.sends, coll, k, nbytes, pre=pre, post=post, n_chunks=n_chunks)
+    assert rep["n_violations"] == 0, rep
     return syn, sch, t
 
 

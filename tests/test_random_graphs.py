@@ -93,6 +93,8 @@ def test_gpu_parity_on_random_graphs(T, inst, coll, literal, seeds):
     t = T.Topology.from_workload_topology(topo)
     sch = T.synthesize(t, coll, k, nbytes, seeds, base, keep_seed_times=True, literal=literal)
     assert_parity(syn, sch, coll)
+    rep = T.evaluate(t, sch.sends, coll, k, nbytes, literal=literal)
+    assert rep["n_violations"] == 0, rep
     if literal:
         assert sch.result["cancelled"] == oracle_literal_stats(syn)
 
