@@ -105,6 +105,10 @@ class tacos_dim_spec(ctypes.Structure):
 
 
 TACOS_DIM_RING, TACOS_DIM_FC, TACOS_DIM_SWITCH, TACOS_DIM_PATH = 0, 1, 2, 3
+
+
+class tacos_tenant(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("root", ctypes.c_uint32), ("k", ctypes.c_uint32)]
 DIM_KINDS = {"ring": TACOS_DIM_RING, "fc": TACOS_DIM_FC, "switch": TACOS_DIM_SWITCH, "path": TACOS_DIM_PATH}
 
 
@@ -162,6 +166,8 @@ SIGNATURES = {
     "tacos_remove_npus": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _I32P, _I32P, _U32P, _U32P, _I32P,
                                          ctypes.c_uint32, _I32P, _I32P, _I32P, _I32P, _U32P, _U32P, ctypes.c_int64,
                                          _I32P]),
+    "tacos_multi_tenant": (ctypes.c_int, [ctypes.c_uint32, ctypes.POINTER(tacos_tenant), ctypes.c_uint32, _U32P,
+                                          _U32P, _U32P, _U32P, ctypes.c_uint64]),
     "tacos_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "tacos_last_error": (ctypes.c_char_p, []),
     "tacos_abi_version": (ctypes.c_int, []),
@@ -593,49 +599,27 @@ def baseline(topo: Topology, algorithm="ring", collective="AR", chunks_per_npu=1
 # multi-tenant collectives (Table VI)
 # --------------------------------------------------------------------------
 def multi_tenant(n_npus: int, tenants) -> Tuple[int, np.ndarray, np.ndarray, list]:
-    """Merge concurrent tenants into one CUSTOM pre/postcondition over disjoint
-    chunk ranges, to be synthesized with relay=True.  tenants: (kind, root, k)
-    with kind AG (root unused), BROADCAST, SCATTER, GATHER or REDUCE; a Reduce
-    tenant inside the merged forward search is scheduled as the Gather of its N
-    partial chunks (reading R23).  Returns (C, pre, post, first chunk
-    id of each tenant); pre/post are N x ceil(C/32) uint32 rows."""
-    n = int(n_npus)
-    spans = []
-    for kind, root, k in tenants:
+    """tacos_multi_tenant: merge concurrent tenants (kind, root, k) -- kind AG (root
+    unused), BROADCAST, SCATTER, GATHER or REDUCE -- into one CUSTOM pre/postcondition
+    over disjoint chunk ranges, to be synthesized with relay=True (reading R23: a Reduce
+    tenant is scheduled as the Gather of its N partial chunks).  Returns (C, pre, post,
+    first chunk id of each tenant); pre/post are N x ceil(C/32) uint32 rows."""
+    lib = load_library()
+    arr = (tacos_tenant * len(tenants))()
+    for a, (kind, root, k) in zip(arr, tenants):
         if kind not in ("AG", "BROADCAST", "SCATTER", "GATHER", "REDUCE"):
             raise ValueError(f"unknown tenant kind {kind}")
-        if kind != "AG" and not 0 <= root < n:
-            raise ValueError("tenant root out of range")
-        spans.append(k if kind == "BROADCAST" else n * k)
-    C = int(sum(spans))
-    words = (C + 31) // 32
-    held = np.zeros((n, C), dtype=bool)
-    need = np.zeros((n, C), dtype=bool)
-    first, base = [], 0
-    for (kind, root, k), span in zip(tenants, spans):
-        first.append(base)
-        ids = np.arange(base, base + span)
-        owner = (ids - base) // k
-        if kind == "AG":
-            held[owner, ids] = True
-            need[:, ids] = True
-        elif kind == "BROADCAST":
-            held[root, ids] = True
-            need[:, ids] = True
-        elif kind == "SCATTER":
-            held[root, ids] = True
-            need[root, ids] = True
-            need[owner, ids] = True
-        else:  # GATHER, REDUCE (R23)
-            held[owner, ids] = True
-            need[owner, ids] = True
-            need[root, ids] = True
-        base += span
-
-    def pack(m):
-        out = np.zeros((n, words), dtype=np.uint32)
-        for c in range(C):
-            out[:, c >> 5] |= (m[:, c].astype(np.uint32) << np.uint32(c & 31))
-        return out
-
-    return C, pack(held), pack(need), first
+        a.kind = COLLECTIVES[kind]
+        a.root = int(root)
+        a.k = int(k)
+    C = ctypes.c_uint32()
+    _check(lib.tacos_multi_tenant(n_npus, arr, len(tenants), ctypes.byref(C), None, None, None, 0),
+           "tacos_multi_tenant")
+    words = (C.value + 31) // 32
+    pre = np.zeros((n_npus, words), np.uint32)
+    post = np.zeros((n_npus, words), np.uint32)
+    first = np.zeros(len(tenants), np.uint32)
+    _check(lib.tacos_multi_tenant(n_npus, arr, len(tenants), ctypes.byref(C), _ptr(pre, ctypes.c_uint32),
+                                  _ptr(post, ctypes.c_uint32), _ptr(first, ctypes.c_uint32), pre.size),
+           "tacos_multi_tenant")
+    return int(C.value), pre, post, [int(x) for x in first]

@@ -1816,6 +1816,66 @@ extern "C" int tacos_remove_npus(int32_t n_npus, int32_t n_links, const int32_t 
 }
 
 // ---------------------------------------------------------------------------
+// Multi-tenant merge (f2; Table VI; reading R23)
+// ---------------------------------------------------------------------------
+extern "C" int tacos_multi_tenant(uint32_t N, const tacos_tenant *tn, uint32_t n_tenants, uint32_t *n_chunks,
+                                  uint32_t *pre, uint32_t *post, uint32_t *first, uint64_t capacity_words) {
+  if (!tn || !n_chunks || n_tenants == 0) return fail(TACOS_E_INVALID_ARG, "null argument or no tenant");
+  if (N < 2) return fail(TACOS_E_INVALID_ARG, "n_npus = %u < 2", N);
+  uint64_t C = 0;
+  for (uint32_t i = 0; i < n_tenants; ++i) {
+    const tacos_tenant &t = tn[i];
+    if (t.kind != TACOS_ALL_GATHER && t.kind != TACOS_BROADCAST && t.kind != TACOS_SCATTER && t.kind != TACOS_GATHER &&
+        t.kind != TACOS_REDUCE)
+      return fail(TACOS_E_INVALID_ARG, "tenant %u: unknown kind %d", i, t.kind);
+    if (t.k < 1) return fail(TACOS_E_INVALID_ARG, "tenant %u: k = 0", i);
+    if (t.kind != TACOS_ALL_GATHER && t.root >= N) return fail(TACOS_E_INVALID_ARG, "tenant %u: root %u >= N", i, t.root);
+    C += t.kind == TACOS_BROADCAST ? (uint64_t)t.k : (uint64_t)N * t.k;
+    if (C > kMaxChunks) return fail(TACOS_E_OVERFLOW, "merged tenants need more than %u chunks", kMaxChunks);
+  }
+  *n_chunks = (uint32_t)C;
+  if (capacity_words == 0) return TACOS_OK;
+  const uint32_t W0 = ((uint32_t)C + 31u) / 32u;
+  if (capacity_words < (uint64_t)N * W0)
+    return fail(TACOS_E_CAPACITY, "capacity %llu < %llu words", (unsigned long long)capacity_words,
+                (unsigned long long)N * W0);
+  if (!pre || !post || !first) return fail(TACOS_E_INVALID_ARG, "null output array");
+  std::memset(pre, 0, sizeof(uint32_t) * (size_t)N * W0);
+  std::memset(post, 0, sizeof(uint32_t) * (size_t)N * W0);
+  auto set = [&](uint32_t *v, uint32_t x, uint32_t c) { v[(size_t)x * W0 + (c >> 5)] |= 1u << (c & 31u); };
+  uint32_t base = 0;
+  for (uint32_t i = 0; i < n_tenants; ++i) {
+    const tacos_tenant &t = tn[i];
+    const uint32_t span = t.kind == TACOS_BROADCAST ? t.k : N * t.k;
+    first[i] = base;
+    for (uint32_t j = 0; j < span; ++j) {
+      const uint32_t c = base + j, owner = j / t.k;
+      switch (t.kind) {
+        case TACOS_ALL_GATHER:
+          set(pre, owner, c);
+          for (uint32_t x = 0; x < N; ++x) set(post, x, c);
+          break;
+        case TACOS_BROADCAST:
+          set(pre, t.root, c);
+          for (uint32_t x = 0; x < N; ++x) set(post, x, c);
+          break;
+        case TACOS_SCATTER:
+          set(pre, t.root, c);
+          set(post, t.root, c);
+          set(post, owner, c);
+          break;
+        default:  // GATHER, REDUCE (R23)
+          set(pre, owner, c);
+          set(post, owner, c);
+          set(post, t.root, c);
+      }
+    }
+    base += span;
+  }
+  return TACOS_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Continuous-time evaluation (f3) and the Ring
 // / Direct baselines.
 // ---------------------------------------------------------------------------

@@ -205,3 +205,30 @@ def test_multi_tenant_table6_shape():
     for e in syn.sends.tolist():
         got[e[2], e[0] >> 5] |= np.uint32(1 << (e[0] & 31))
     assert np.all((post & ~got) == 0)
+
+
+@pytest.mark.parametrize("n,tenants", [
+    (36, [("BROADCAST", 2, 1), ("REDUCE", 17, 1), ("AG", 0, 1)]),
+    (16, [("SCATTER", 3, 2), ("GATHER", 15, 1), ("BROADCAST", 0, 5)]),
+    (9, [("AG", 0, 3), ("AG", 0, 1), ("REDUCE", 8, 2), ("SCATTER", 4, 1)]),
+    (2, [("GATHER", 1, 7)]),
+])
+def test_multi_tenant_abi_matches_oracle(T, n, tenants):
+    """tacos_multi_tenant (C ABI) builds the same merged pre/post as the oracle's
+    plain-numpy merge (Table VI; R23)."""
+    C, pre, post, first = OC.multi_tenant(n, tenants)
+    C2, pre2, post2, first2 = T.multi_tenant(n, tenants)
+    assert (C2, first2) == (C, first)
+    assert np.array_equal(pre2, pre) and np.array_equal(post2, post)
+
+
+def test_multi_tenant_abi_errors(T):
+    with pytest.raises(T.TacosError) as e:
+        T.multi_tenant(4, [("BROADCAST", 4, 1)])
+    assert e.value.code == T.TACOS_E_INVALID_ARG
+    with pytest.raises(T.TacosError) as e:
+        T.multi_tenant(4, [("AG", 0, 0)])
+    assert e.value.code == T.TACOS_E_INVALID_ARG
+    with pytest.raises(T.TacosError) as e:
+        T.multi_tenant(1024, [("AG", 0, 8), ("AG", 0, 9)])
+    assert e.value.code == T.TACOS_E_OVERFLOW

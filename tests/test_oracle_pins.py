@@ -107,6 +107,42 @@ def test_first_event_draws_follow_curand_stream(seed):
     assert res.T == 5
 
 
+@pytest.mark.parametrize("seed", [3, 0xFEEDFACE, 2**63 + 5])
+def test_first_event_select_across_words_follows_curand_stream(seed):
+    """Cross-word rank-select (R12, R13): a star, link i = 0 -> i+1 (i < 24), one
+    in-link per destination.  NPU 0 holds a random set S of the C = 160 chunks
+    (5 words), NPU i+1 a random set H_i.  At t = 0 link i takes the r-th smallest
+    member of S - H_i with r = floor(word1 * K / 2^32), K = |S - H_i|, word1 of
+    cuRAND's block i (counter (0, 0, i, 0)).  The expected chunk is computed from
+    cuRAND's stream and a sorted Python list, not from the oracle; the candidate
+    sets span every word, so a slip in the word walk changes the outcome."""
+    n_links, C = 24, 160
+    rng = np.random.default_rng(seed % 2**32)
+    S = sorted(set(rng.choice(C, 90, replace=False).tolist()))
+    H = [set(rng.choice(C, int(rng.integers(0, 60)), replace=False).tolist()) for _ in range(n_links)]
+    blocks = _curand_blocks(seed, n_links)
+    pre_sets = {0: S}
+    post_sets = {0: S}
+    for i in range(n_links):
+        pre_sets[i + 1] = sorted(H[i])
+        post_sets[i + 1] = sorted(set(S) | H[i])
+    n = n_links + 1
+    pre = oracle.bits_from_sets(n, C, pre_sets)
+    post = oracle.bits_from_sets(n, C, post_sets)
+    src = np.zeros(n_links, np.int32)
+    dst = np.arange(1, n, dtype=np.int32)
+    w = np.full(n_links, 7, np.uint64)
+    res = oracle.greedy(n, src, dst, w, C, 1, seed, 0, pre, post)
+    first = {int(e["link"]): int(e["chunk"]) for e in res.sends if int(e["t_start"]) == 0}
+    words_hit = set()
+    for i in range(n_links):
+        cand = [c for c in S if c not in H[i]]
+        r = (int(blocks[i, 1]) * len(cand)) >> 32
+        assert first[i] == cand[r], (i, first[i], cand[r])
+        words_hit.add(cand[r] >> 5)
+    assert words_hit == set(range(C // 32))  # the picks land in every word
+
+
 # --------------------------------------------------------------------------
 # a1 cost quantization (P:L104, P:L172; R5, R6)
 # --------------------------------------------------------------------------
