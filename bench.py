@@ -232,6 +232,14 @@ def run_gpu(args):
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     T.load_library()
+    comm = None
+    if world > 1:
+        # the exchange step of best-of-S runs inside the library (tacos_plan_allreduce_keys:
+        # ncclAllReduce MIN over NVLink); torch.distributed only ships the NCCL id, the barriers
+        # and the max-over-ranks timing
+        obj = [T.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = T.Comm(obj[0], world, rank)
     wl = workload(args.config, args.seeds)
     S = wl.n_seeds
     C = wl.topo.n_npus * wl.chunks_per_npu
@@ -241,7 +249,6 @@ def run_gpu(args):
     plan = T.Plan(topo, wl.collective, wl.chunks_per_npu, wl.chunk_bytes, S, 0, rank * S, literal=args.literal)
     n_sends = plan.n_sends
     d_sends = torch.empty(n_sends * 32, dtype=torch.uint8, device="cuda")
-    keys = plan.best_keys_tensor()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def barrier():
@@ -255,7 +262,7 @@ def run_gpu(args):
             plan.search(sh)
             ev[1].record(stream)
             if world > 1:
-                dist.all_reduce(keys, op=dist.ReduceOp.MIN)
+                plan.allreduce_keys(comm, sh)
             res = plan.emit(d_sends.data_ptr(), n_sends, sh)
             ev[2].record(stream)
         return res
@@ -334,7 +341,7 @@ def run_gpu(args):
             pl = T.Plan(tt, wl.collective, wl.chunks_per_npu, wl.chunk_bytes, S, 0, rank * S)
             with torch.cuda.stream(stream):
                 pl.search(sh)
-                dist.all_reduce(pl.best_keys_tensor(), op=dist.ReduceOp.MIN)
+                pl.allreduce_keys(comm, sh)
                 r = pl.emit(d_sends.data_ptr(), n_sends, sh)
                 if r["winner_local"]:
                     host_out.copy_(d_sends, non_blocking=True)

@@ -67,7 +67,7 @@ class tacos_synth_params(ctypes.Structure):
                 ("time_unit_ns", ctypes.c_uint32), ("n_seeds", ctypes.c_uint32), ("base_seed", ctypes.c_uint64),
                 ("seed_offset", ctypes.c_uint32), ("n_chunks", ctypes.c_uint32),
                 ("pre_bits", ctypes.POINTER(ctypes.c_uint32)), ("post_bits", ctypes.POINTER(ctypes.c_uint32)),
-                ("flags", ctypes.c_uint32), ("root", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("root", ctypes.c_uint32), ("n_devices", ctypes.c_uint32)]
 
 
 class tacos_result(ctypes.Structure):
@@ -166,6 +166,12 @@ SIGNATURES = {
     "tacos_remove_npus": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _I32P, _I32P, _U32P, _U32P, _I32P,
                                          ctypes.c_uint32, _I32P, _I32P, _I32P, _I32P, _U32P, _U32P, ctypes.c_int64,
                                          _I32P]),
+    "tacos_comm_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
+    "tacos_comm_init_rank": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8), ctypes.c_int32, ctypes.c_int32,
+                                            ctypes.POINTER(_VP)]),
+    "tacos_comm_destroy": (None, [_VP]),
+    "tacos_plan_allreduce_keys": (ctypes.c_int, [_VP, _VP, _VP]),
+    "tacos_nccl_version": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),
     "tacos_multi_tenant": (ctypes.c_int, [ctypes.c_uint32, ctypes.POINTER(tacos_tenant), ctypes.c_uint32, _U32P,
                                           _U32P, _U32P, _U32P, ctypes.c_uint64]),
     "tacos_strerror": (ctypes.c_char_p, [ctypes.c_int]),
@@ -235,10 +241,12 @@ def tacos_free_topology(h):
 
 
 def make_params(collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=1, base_seed=0, seed_offset=0,
-                time_unit_ns=1, flags=0, pre=None, post=None, n_chunks=0, root=0) -> Tuple[tacos_synth_params, tuple]:
+                time_unit_ns=1, flags=0, pre=None, post=None, n_chunks=0, root=0,
+                n_devices=0) -> Tuple[tacos_synth_params, tuple]:
     """Build tacos_synth_params; returns (params, keepalive)."""
     p = tacos_synth_params()
     p.root = root
+    p.n_devices = n_devices
     p.collective = COLLECTIVES[collective] if isinstance(collective, str) else int(collective)
     p.chunks_per_npu = chunks_per_npu
     p.chunk_bytes = chunk_bytes
@@ -388,13 +396,13 @@ class Schedule:
 
 def synthesize(topo: Topology, collective="AR", chunks_per_npu=1, chunk_bytes=1 << 20, n_seeds=1, base_seed=0,
                time_unit_ns=1, keep_seed_times=False, no_schedule=False, pre=None, post=None,
-               n_chunks=0, literal=False, relay=False, root=0) -> Schedule:
+               n_chunks=0, literal=False, relay=False, root=0, n_devices=0) -> Schedule:
     """tacos_synthesize.  collective: AG / RS / AR / CUSTOM (pre, post, n_chunks; relay=True
     for relays, R22) or the rooted BROADCAST / REDUCE / SCATTER / GATHER (root)."""
     flags = ((TACOS_FLAG_KEEP_SEED_TIMES if keep_seed_times else 0) | (TACOS_FLAG_NO_SCHEDULE if no_schedule else 0)
              | (TACOS_FLAG_LITERAL if literal else 0) | (TACOS_FLAG_RELAY if relay else 0))
     p, keep = make_params(collective, chunks_per_npu, chunk_bytes, n_seeds, base_seed, 0, time_unit_ns, flags, pre,
-                          post, n_chunks, root)
+                          post, n_chunks, root, n_devices)
     h = tacos_synthesize(topo.handle, p)
     try:
         sends = tacos_schedule_sends(h)
@@ -411,7 +419,8 @@ def synthesize_batch(topos: Sequence[Topology], **kw) -> list:
     keep_times = kw.pop("keep_seed_times", False)
     flags = TACOS_FLAG_KEEP_SEED_TIMES if keep_times else 0
     p, keep = make_params(kw.get("collective", "AR"), kw.get("chunks_per_npu", 1), kw.get("chunk_bytes", 1 << 20),
-                          n_seeds, kw.get("base_seed", 0), 0, kw.get("time_unit_ns", 1), flags)
+                          n_seeds, kw.get("base_seed", 0), 0, kw.get("time_unit_ns", 1), flags,
+                          n_devices=kw.get("n_devices", 0))
     hs = tacos_synthesize_batch([t.handle for t in topos], p)
     out = []
     for h in hs:
@@ -477,6 +486,11 @@ class Plan:
     def search(self, stream: int = 0):
         _check(load_library().tacos_plan_search(self.handle, ctypes.c_void_p(stream)), "tacos_plan_search")
 
+    def allreduce_keys(self, comm: "Comm", stream: int = 0):
+        """tacos_plan_allreduce_keys: the cross-rank MIN of the best keys over NCCL."""
+        _check(load_library().tacos_plan_allreduce_keys(self.handle, comm.handle, ctypes.c_void_p(stream)),
+               "tacos_plan_allreduce_keys")
+
     def best_keys_ptr(self) -> int:
         return int(load_library().tacos_plan_best_keys(self.handle))
 
@@ -509,6 +523,38 @@ class Plan:
         h = getattr(self, "handle", None)
         if h is not None and _lib is not None:
             _lib.tacos_plan_destroy(h)
+            self.handle = None
+
+
+COMM_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    """tacos_comm_unique_id (rank 0), 128 bytes to ship to the other ranks."""
+    buf = (ctypes.c_uint8 * COMM_ID_BYTES)()
+    _check(load_library().tacos_comm_unique_id(buf), "tacos_comm_unique_id")
+    return bytes(buf)
+
+
+def nccl_version() -> int:
+    v = ctypes.c_int32()
+    _check(load_library().tacos_nccl_version(ctypes.byref(v)), "tacos_nccl_version")
+    return int(v.value)
+
+
+class Comm:
+    """tacos_comm: one rank of a multi-process job, on the current CUDA device."""
+
+    def __init__(self, unique_id: bytes, n_ranks: int, rank: int):
+        buf = (ctypes.c_uint8 * COMM_ID_BYTES).from_buffer_copy(unique_id)
+        h = ctypes.c_void_p()
+        _check(load_library().tacos_comm_init_rank(buf, n_ranks, rank, ctypes.byref(h)), "tacos_comm_init_rank")
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.tacos_comm_destroy(h)
             self.handle = None
 
 

@@ -10,8 +10,8 @@ INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libtacos.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["tacos_kernels.cu", "tacos_api.cpp", "literal_kernel.cu"] + [f"greedy_p{p}.cu" for p in (1, 2, 4, 8, 16, 32)]
-HEADERS = ["tacos_internal.h", "tacos_device.cuh", "greedy_kernel.cuh", os.path.join(INC, "tacos.h")]
+SOURCES = ["tacos_kernels.cu", "tacos_api.cpp", "tacos_nccl.cpp", "literal_kernel.cu"] + [f"greedy_p{p}.cu" for p in (1, 2, 4, 8, 16, 32)]
+HEADERS = ["tacos_internal.h", "tacos_nccl.h", "tacos_device.cuh", "greedy_kernel.cuh", os.path.join(INC, "tacos.h")]
 
 
 def _stale() -> bool:

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -25,6 +27,7 @@
 #include <vector>
 
 #include "tacos_internal.h"
+#include "tacos_nccl.h"
 
 using namespace tacos;
 
@@ -152,26 +155,39 @@ struct tacos_topology {
   bool strongly_connected = false;
   // orientation 0 = G (grouped by dst), 1 = G^T (grouped by src)
   std::vector<uint32_t> in_ptr[2], pos_lid[2], pos_src[2], pos_dst[2];
-  int device = -1;
-  uint32_t *d_in_ptr[2] = {nullptr, nullptr}, *d_pos_lid[2] = {nullptr, nullptr};
-  uint32_t *d_pos_src[2] = {nullptr, nullptr}, *d_pos_dst[2] = {nullptr, nullptr};
-  uint32_t *d_src = nullptr, *d_dst = nullptr;
-  int32_t *d_rev = nullptr;
-  std::vector<DevBuf> bufs;
+  int device = -1;  // device current at load time (its copy is uploaded eagerly), -1 without a GPU
+  // per-device copies of the CSR arrays (tacos_synthesize with n_devices > 1 uses several),
+  // created on first use under the mutex; the handle stays logically immutable
+  struct Dev {
+    int dev = -1;
+    uint32_t *d_in_ptr[2] = {nullptr, nullptr}, *d_pos_lid[2] = {nullptr, nullptr};
+    uint32_t *d_pos_src[2] = {nullptr, nullptr}, *d_pos_dst[2] = {nullptr, nullptr};
+    uint32_t *d_src = nullptr, *d_dst = nullptr;
+    int32_t *d_rev = nullptr;
+    std::vector<DevBuf> bufs;
+  };
+  mutable std::mutex mu;
+  mutable std::vector<std::unique_ptr<Dev>> devs;
   ~tacos_topology() {
     // the blocks go back to a caching pool (no implicit synchronization as with cudaFree):
     // wait for every kernel that may still read them (a plan built from this topology)
-    if (!bufs.empty()) {
-      int cur = -1;
-      if (cudaGetDevice(&cur) == cudaSuccess && cudaSetDevice(device) == cudaSuccess) {
-        cudaDeviceSynchronize();
-        cudaSetDevice(cur);
-      }
-      cudaGetLastError();
+    int cur = -1;
+    const bool have_cur = cudaGetDevice(&cur) == cudaSuccess;
+    for (auto &d : devs) {
+      if (cudaSetDevice(d->dev) == cudaSuccess) cudaDeviceSynchronize();
+      for (auto &b : d->bufs) device_pool().release(b.dev, b.p, b.cls);
     }
-    for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
+    if (have_cur) cudaSetDevice(cur);
+    cudaGetLastError();
   }
 };
+using TopoDev = tacos_topology::Dev;
+
+namespace {
+// The topology's arrays on device `dev` (the calling thread's current device), uploaded on
+// first use (one pinned staging copy + one H2D copy, synchronous).
+int topo_on_device(const tacos_topology *t, int dev, const TopoDev **out);
+}  // namespace
 
 namespace {
 template <typename T>
@@ -294,6 +310,57 @@ bool symmetric_for(const tacos_topology *t, const std::vector<uint32_t> &w) {
 }
 }  // namespace
 
+namespace {
+int topo_on_device(const tacos_topology *t, int dev, const TopoDev **out) {
+  std::lock_guard<std::mutex> g(t->mu);
+  for (auto &d : t->devs)
+    if (d->dev == dev) {
+      *out = d.get();
+      return TACOS_OK;
+    }
+  std::unique_ptr<TopoDev> d(new TopoDev());
+  d->dev = dev;
+  Stager sg;
+  const size_t lb = (size_t)t->L * 4;
+  size_t o_ptr[2], o_lid[2], o_src[2], o_dst[2];
+  for (int o = 0; o < 2; ++o) {
+    o_ptr[o] = sg.reserve(t->in_ptr[o].size() * 4);
+    o_lid[o] = sg.reserve(lb);
+    o_src[o] = sg.reserve(lb);
+    o_dst[o] = sg.reserve(lb);
+  }
+  const size_t o_s = sg.reserve(lb), o_d = sg.reserve(lb), o_r = sg.reserve(lb);
+  int rc;
+  if ((rc = sg.alloc(d->bufs, dev))) {
+    for (auto &b : d->bufs) device_pool().release(b.dev, b.p, b.cls);
+    return rc;
+  }
+  for (int o = 0; o < 2; ++o) {
+    sg.put(o_ptr[o], t->in_ptr[o].data(), t->in_ptr[o].size() * 4);
+    sg.put(o_lid[o], t->pos_lid[o].data(), lb);
+    sg.put(o_src[o], t->pos_src[o].data(), lb);
+    sg.put(o_dst[o], t->pos_dst[o].data(), lb);
+    d->d_in_ptr[o] = sg.at<uint32_t>(o_ptr[o]);
+    d->d_pos_lid[o] = sg.at<uint32_t>(o_lid[o]);
+    d->d_pos_src[o] = sg.at<uint32_t>(o_src[o]);
+    d->d_pos_dst[o] = sg.at<uint32_t>(o_dst[o]);
+  }
+  sg.put(o_s, t->src.data(), lb);  // int32 ids < 2^31: the same bytes as uint32
+  sg.put(o_d, t->dst.data(), lb);
+  sg.put(o_r, t->rev.data(), lb);
+  d->d_src = sg.at<uint32_t>(o_s);
+  d->d_dst = sg.at<uint32_t>(o_d);
+  d->d_rev = sg.at<int32_t>(o_r);
+  if ((rc = sg.copy_sync(dev, nullptr))) {
+    for (auto &b : d->bufs) device_pool().release(b.dev, b.p, b.cls);
+    return rc;
+  }
+  *out = d.get();
+  t->devs.push_back(std::move(d));
+  return TACOS_OK;
+}
+}  // namespace
+
 extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_t *src, const int32_t *dst,
                                    const uint32_t *alpha_ns, const uint32_t *bw, tacos_topology **out) {
   if (out) *out = nullptr;
@@ -361,35 +428,9 @@ extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_
   int n = 0;
   if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) {
     t->device = dev;
-    int rc;
-    Stager sg;
-    const size_t lb = (size_t)n_links * 4;
-    size_t o_ptr[2], o_lid[2], o_src[2], o_dst[2];
-    for (int o = 0; o < 2; ++o) {
-      o_ptr[o] = sg.reserve(t->in_ptr[o].size() * 4);
-      o_lid[o] = sg.reserve(lb);
-      o_src[o] = sg.reserve(lb);
-      o_dst[o] = sg.reserve(lb);
-    }
-    const size_t o_s = sg.reserve(lb), o_d = sg.reserve(lb), o_r = sg.reserve(lb);
-    if ((rc = sg.alloc(t->bufs, dev))) return rc;
-    for (int o = 0; o < 2; ++o) {
-      sg.put(o_ptr[o], t->in_ptr[o].data(), t->in_ptr[o].size() * 4);
-      sg.put(o_lid[o], t->pos_lid[o].data(), lb);
-      sg.put(o_src[o], t->pos_src[o].data(), lb);
-      sg.put(o_dst[o], t->pos_dst[o].data(), lb);
-      t->d_in_ptr[o] = sg.at<uint32_t>(o_ptr[o]);
-      t->d_pos_lid[o] = sg.at<uint32_t>(o_lid[o]);
-      t->d_pos_src[o] = sg.at<uint32_t>(o_src[o]);
-      t->d_pos_dst[o] = sg.at<uint32_t>(o_dst[o]);
-    }
-    sg.put(o_s, src, lb);  // int32 ids < 2^31: the same bytes as uint32
-    sg.put(o_d, dst, lb);
-    sg.put(o_r, t->rev.data(), lb);
-    t->d_src = sg.at<uint32_t>(o_s);
-    t->d_dst = sg.at<uint32_t>(o_d);
-    t->d_rev = sg.at<int32_t>(o_r);
-    if ((rc = sg.copy_sync(dev, nullptr))) return rc;
+    const TopoDev *td = nullptr;
+    int rc = topo_on_device(t.get(), dev, &td);
+    if (rc) return rc;
   } else {
     cudaGetLastError();
   }
@@ -424,6 +465,7 @@ extern "C" int tacos_is_symmetric(const tacos_topology *t, uint64_t chunk_bytes,
 namespace {
 struct Part {
   const tacos_topology *topo = nullptr;
+  const TopoDev *td = nullptr;  // the topology's arrays on the plan's device
   uint32_t N = 0, L = 0, C = 0, k = 0, Wp = 0, P = 0, VPL = 0;
   bool custom = false, symmetric = false, rs_search = false;
   uint32_t rs_base = 0;  // first job of the G^T (sigma 1) search: S, or 0 when only the RS phase is searched
@@ -652,9 +694,9 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   for (uint32_t i = 0; i < n_topos; ++i) {
     const tacos_topology *t = topos[i];
     if (!t) return fail(TACOS_E_INVALID_ARG, "null topology %u", i);
-    if (t->device != dev) return fail(TACOS_E_CUDA, "topology %u was loaded on device %d, current device %d", i, t->device, dev);
     Part &pt = pl->parts[i];
     pt.topo = t;
+    if ((rc = topo_on_device(t, dev, &pt.td))) return rc;
     pt.N = (uint32_t)t->N;
     pt.L = (uint32_t)t->L;
     pt.custom = custom;
@@ -867,11 +909,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       h.VPL = pt.VPL;
       h.custom = custom ? 1u : 0u;
       h.required = pt.required;
-      h.in_ptr = t->d_in_ptr[o];
-      h.p_src = t->d_pos_src[o];
-      h.p_dst = t->d_pos_dst[o];
+      h.in_ptr = pt.td->d_in_ptr[o];
+      h.p_src = pt.td->d_pos_src[o];
+      h.p_dst = pt.td->d_pos_dst[o];
       h.p_w = d_pos_w[o];
-      h.p_lid = t->d_pos_lid[o];
+      h.p_lid = pt.td->d_pos_lid[o];
       h.pre = d_pre;
       h.post = d_post;
       h.allow = d_allow[o];
@@ -1014,7 +1056,7 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   res->T = win.T;
   res->rs_seed = pl->p.base_seed + g_rs;
   res->seed = need_ag ? pl->p.base_seed + g_ag : res->rs_seed;
-  const uint32_t S = pl->p.n_seeds, off = pl->p.seed_offset;
+  const uint32_t off = pl->p.seed_offset;
   const bool ag_local = (win.local & 1u) != 0;
   const bool rs_local = (win.local & 2u) != 0;
   res->winner_local = win.local;
@@ -1022,7 +1064,6 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   const uint64_t nsend = sends_per_result(pl, pt);
   if (nsend == 0) return TACOS_OK;
   if (capacity < nsend) return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)capacity, (unsigned long long)nsend);
-  const tacos_topology *t = pt.topo;
   int rc;
   uint64_t emitted = 0;
   // matches of a winning job: `required` without relays, else read back from its JobOut
@@ -1062,10 +1103,10 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
                          (size_t)8 * ((pt.L + 31u) / 32u) <= (size_t)200 * 1024 &&
                          std::all_of(pt.w.begin(), pt.w.end(), [&](uint32_t x) { return x == pt.w[0]; });
     if (uniform) {
-      if ((rc = launch_rs_uniform_emit(rec, M, t->d_src, t->d_dst, pt.w[0], t->d_rev, T_rs, pt.L, d_sends, pl->d_sort,
+      if ((rc = launch_rs_uniform_emit(rec, M, pt.td->d_src, pt.td->d_dst, pt.w[0], pt.td->d_rev, T_rs, pt.L, d_sends, pl->d_sort,
                                        pl->sort_bytes, &nl, st)))
         return fail(rc, "%s", cuda_error_string());
-    } else if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, pt.symmetric ? t->d_rev : nullptr, T_rs,
+    } else if ((rc = launch_rs_sort_emit(rec, M, pt.td->d_src, pt.td->d_dst, pt.d_w, pt.symmetric ? pt.td->d_rev : nullptr, T_rs,
                                          pt.L, d_sends, pl->d_sort, pl->sort_bytes, &nl, st)))
       return fail(rc, "%s", cuda_error_string());
     pl->last_launches += nl;
@@ -1079,12 +1120,12 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
     const uint64_t base = coll == TACOS_ALL_REDUCE ? pt.required : 0;  // AR: after the RS half (no relays)
     if (pl->p.flags & TACOS_FLAG_LITERAL) {  // records in delivery order: sort by (t_start, link)
       uint32_t nl = 0;
-      if ((rc = launch_rs_sort_emit(rec, M, t->d_src, t->d_dst, pt.d_w, nullptr, T_ag, pt.L, d_sends + base, pl->d_sort,
+      if ((rc = launch_rs_sort_emit(rec, M, pt.td->d_src, pt.td->d_dst, pt.d_w, nullptr, T_ag, pt.L, d_sends + base, pl->d_sort,
                                     pl->sort_bytes, &nl, st, /*mirror=*/0u, /*shift=*/T_rs)))
         return fail(rc, "%s", cuda_error_string());
       pl->last_launches += nl;
     } else {
-      if ((rc = launch_emit_ag(rec, M, t->d_src, t->d_dst, pt.d_w, T_rs, d_sends + base, st, T_rs + T_ag)))
+      if ((rc = launch_emit_ag(rec, M, pt.td->d_src, pt.td->d_dst, pt.d_w, T_rs, d_sends + base, st, T_rs + T_ag)))
         return fail(rc, "%s", cuda_error_string());
       pl->last_launches += 1;
     }
@@ -1231,6 +1272,33 @@ bool is_device_ptr(const void *ptr) {
 
 // Search + emit for n_topos topologies; per topology: sends into dst[i] (host or
 // device, capacity caps[i]) and results[i]; seed times optional.
+// Per-seed collective times (tacos_schedule_seed_times) of a part from the AG-on-G and
+// AG-on-G^T search times: AG-type T_AG(s); RS-type T_RS(s); AR T_RS(s) + T_AG(s) (R10),
+// where on a symmetric graph T_RS(s) = T_AG(s) (R9).
+void combine_seed_times(const Part &pt, int coll, uint32_t S, const std::vector<uint64_t> &t_ag,
+                        const std::vector<uint64_t> &t_rs, uint64_t *out) {
+  const bool fwd_jobs = !pt.rs_search || pt.rs_base > 0;
+  for (uint32_t s = 0; s < S; ++s) {
+    const uint64_t ta = fwd_jobs ? t_ag[s] : 0, tr = pt.rs_search ? t_rs[s] : ta;
+    out[s] = !coll_need_rs(coll) ? ta : (coll == TACOS_ALL_REDUCE ? tr + ta : tr);
+  }
+}
+
+// D2H of a part's per-seed search times (async on st; read after a synchronize)
+int read_seed_times_async(const Part &pt, uint32_t S, std::vector<uint64_t> &t_ag, std::vector<uint64_t> &t_rs,
+                          cudaStream_t st) {
+  const bool fwd_jobs = !pt.rs_search || pt.rs_base > 0;
+  if (fwd_jobs) {
+    t_ag.resize(S);
+    CUDA_TRY(cudaMemcpyAsync(t_ag.data(), pt.d_times_ag, 8 * (size_t)S, cudaMemcpyDeviceToHost, st));
+  }
+  if (pt.rs_search) {
+    t_rs.resize(S);
+    CUDA_TRY(cudaMemcpyAsync(t_rs.data(), pt.d_times_rs, 8 * (size_t)S, cudaMemcpyDeviceToHost, st));
+  }
+  return TACOS_OK;
+}
+
 int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p, tacos_send **dst,
                const uint64_t *caps, tacos_result *results, std::vector<uint64_t> *seed_times, cudaStream_t st) {
   tacos_plan *raw = nullptr;
@@ -1275,19 +1343,7 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     // per-seed collective times (tacos_schedule_seed_times): AG-type T_AG(s); RS-type T_RS(s);
     // AR T_RS(s) + T_AG(s) (R10), where on a symmetric graph T_RS(s) = T_AG(s) (R9)
     std::vector<uint64_t> t_ag, t_rs;
-    const bool fwd_jobs = !pt.rs_search || pt.rs_base > 0;
-    if (rc == TACOS_OK && seed_times) {
-      cudaError_t e = cudaSuccess;
-      if (fwd_jobs) {
-        t_ag.resize(p->n_seeds);
-        e = cudaMemcpyAsync(t_ag.data(), pt.d_times_ag, 8 * (size_t)p->n_seeds, cudaMemcpyDeviceToHost, st);
-      }
-      if (e == cudaSuccess && pt.rs_search) {
-        t_rs.resize(p->n_seeds);
-        e = cudaMemcpyAsync(t_rs.data(), pt.d_times_rs, 8 * (size_t)p->n_seeds, cudaMemcpyDeviceToHost, st);
-      }
-      if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "D2H of seed times: %s", cudaGetErrorString(e));
-    }
+    if (rc == TACOS_OK && seed_times) rc = read_seed_times_async(pt, p->n_seeds, t_ag, t_rs, st);
     if (rc == TACOS_OK) {
       cudaError_t e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "synchronize: %s", cudaGetErrorString(e));
@@ -1295,14 +1351,185 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     if (tmp.p) device_pool().release(tmp.dev, tmp.p, tmp.cls);
     if (rc) return rc;
     if (seed_times) {
-      const int coll = p->collective;
-      auto &out = seed_times[i];
-      out.resize(p->n_seeds);
-      for (uint32_t s = 0; s < p->n_seeds; ++s) {
-        const uint64_t ta = fwd_jobs ? t_ag[s] : 0, tr = pt.rs_search ? t_rs[s] : ta;
-        out[s] = !coll_need_rs(coll) ? ta : (coll == TACOS_ALL_REDUCE ? tr + ta : tr);
+      seed_times[i].resize(p->n_seeds);
+      combine_seed_times(pt, p->collective, p->n_seeds, t_ag, t_rs, seed_times[i].data());
+    }
+  }
+  return TACOS_OK;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// several GPUs of one process: seed sharding + one NCCL MIN
+// ---------------------------------------------------------------------------
+namespace {
+int resolve_devices(const tacos_synth_params *p, uint32_t *D) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return fail(TACOS_E_CUDA, "no CUDA device available");
+  }
+  uint32_t want = p->n_devices == TACOS_ALL_DEVICES ? (uint32_t)n : p->n_devices;
+  if (want <= 1) want = 1;
+  if (want > (uint32_t)n) return fail(TACOS_E_INVALID_ARG, "n_devices = %u but %d devices are visible", want, n);
+  *D = want;
+  return TACOS_OK;
+}
+
+// NCCL communicators over devices 0 .. D-1 (ncclCommInitAll), created on first use and
+// kept for the life of the process (creation costs far more than a synthesis).
+int nccl_clique(uint32_t D, const NcclApi *api, std::vector<ncclComm_t> **out) {
+  static std::mutex mu;
+  static std::map<uint32_t, std::vector<ncclComm_t>> *cliques = new std::map<uint32_t, std::vector<ncclComm_t>>();
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cliques->find(D);
+  if (it == cliques->end()) {
+    std::vector<ncclComm_t> comms(D);
+    std::vector<int> devs(D);
+    for (uint32_t i = 0; i < D; ++i) devs[i] = (int)i;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    const ncclResult_t r = api->CommInitAll(comms.data(), (int)D, devs.data());
+    cudaSetDevice(cur);
+    if (r != ncclSuccess) return fail(TACOS_E_NCCL, "ncclCommInitAll(%u): %s", D, api->GetErrorString(r));
+    it = cliques->emplace(D, std::move(comms)).first;
+  }
+  *out = &it->second;
+  return TACOS_OK;
+}
+
+// All threads of a sharded synthesis meet here before the collective: a failure on one
+// device must not leave the others waiting inside ncclAllReduce.
+struct Rendezvous {
+  std::mutex m;
+  std::condition_variable cv;
+  uint32_t n, arrived = 0;
+  bool failed = false;
+  explicit Rendezvous(uint32_t n_) : n(n_) {}
+  bool arrive(bool fail_here) {
+    std::unique_lock<std::mutex> lk(m);
+    failed = failed || fail_here;
+    if (++arrived == n) cv.notify_all();
+    else cv.wait(lk, [&] { return arrived == n; });
+    return !failed;
+  }
+};
+
+struct ShardOut {
+  int rc = 0;
+  std::string err;
+  tacos_result res{};
+  std::vector<uint64_t> times;  // the shard's per-seed collective times
+};
+
+// One topology, the seeds sharded over devices 0 .. G-1: each device's thread builds its
+// plan (seed block [g S / G, (g+1) S / G)), searches on its own stream, takes part in one
+// ncclAllReduce(MIN) of the two best keys, and emits the phases whose winning seed it
+// owns into `dst` (host or device memory, same offsets as a one-device emission).
+int synth_sharded(const tacos_topology *topo, const tacos_synth_params *p, uint32_t D, tacos_send *dst, uint64_t cap,
+                  tacos_result *result, std::vector<uint64_t> *seed_times) {
+  const uint32_t S = p->n_seeds, G = std::min(D, S);
+  std::string nerr;
+  const NcclApi *api = nccl_api(&nerr);
+  if (!api) return fail(TACOS_E_NCCL, "%s", nerr.c_str());
+  std::vector<ncclComm_t> *comms = nullptr;
+  int rc = nccl_clique(G, api, &comms);
+  if (rc) return rc;
+  uint64_t need = 0;
+  if ((rc = tacos_max_sends(topo, p, &need))) return rc;
+  if (cap < need) return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)cap, (unsigned long long)need);
+  int caller = 0;
+  CUDA_TRY(cudaGetDevice(&caller));
+  std::vector<ShardOut> outs(G);
+  Rendezvous rv(G);
+  auto work = [&](uint32_t g) {
+    ShardOut &o = outs[g];
+    int r = TACOS_OK;
+    cudaStream_t st = nullptr;
+    tacos_plan *raw = nullptr;
+    tacos_synth_params pg = *p;
+    pg.n_devices = 1;
+    const uint32_t lo = (uint32_t)((uint64_t)g * S / G), hi = (uint32_t)((uint64_t)(g + 1) * S / G);
+    pg.seed_offset = p->seed_offset + lo;
+    pg.n_seeds = hi - lo;
+    if (cudaSetDevice((int)g) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+      r = fail(TACOS_E_CUDA, "device %u: %s", g, cudaGetErrorString(cudaGetLastError()));
+    if (!r) r = plan_build(&topo, 1, &pg, &raw);
+    std::unique_ptr<tacos_plan> pl(raw);
+    if (!r) r = plan_search(pl.get(), st);
+    const bool go = rv.arrive(r != 0);
+    if (go) {
+      uint64_t *keys = pl->parts[0].d_keys;
+      const ncclResult_t nr = api->AllReduce(keys, keys, 2, ncclUint64, ncclMin, (*comms)[g], st);
+      if (nr != ncclSuccess) r = fail(TACOS_E_NCCL, "ncclAllReduce: %s", api->GetErrorString(nr));
+    }
+    if (go && !r) r = plan_read_small(pl.get(), st);
+    DevBuf tmp;
+    std::vector<uint64_t> t_ag, t_rs;
+    if (go && !r) {
+      const Part &pt = pl->parts[0];
+      const uint64_t n_out = sends_per_result(pl.get(), pt);
+      tacos_send *d_out = nullptr;
+      if (n_out) {
+        tmp.dev = (int)g;
+        tmp.p = device_pool().alloc((int)g, n_out * sizeof(tacos_send), &tmp.cls);
+        if (!tmp.p) r = fail(TACOS_E_NOMEM, "device allocation failed");
+        d_out = reinterpret_cast<tacos_send *>(tmp.p);
+      }
+      if (!r) r = plan_emit_part(pl.get(), 0, d_out, n_out, &o.res, st);
+      if (!r && n_out && o.res.winner_local) {  // copy the phases emitted here (same offsets)
+        auto copy = [&](uint64_t off, uint64_t n) {
+          if (!r && n && cudaMemcpyAsync(dst + off, d_out + off, n * sizeof(tacos_send), cudaMemcpyDefault, st) != cudaSuccess)
+            r = fail(TACOS_E_CUDA, "copy of the schedule: %s", cudaGetErrorString(cudaGetLastError()));
+        };
+        if (p->collective == TACOS_ALL_REDUCE) {  // RS half [0, M), AG half [M, 2M) (no relays)
+          if (o.res.winner_local & 2u) copy(0, pt.required);
+          if (o.res.winner_local & 1u) copy(pt.required, pt.required);
+        } else {
+          copy(0, o.res.n_sends);
+        }
+      }
+      if (!r && seed_times) r = read_seed_times_async(pt, pg.n_seeds, t_ag, t_rs, st);
+      if (!r && cudaStreamSynchronize(st) != cudaSuccess)
+        r = fail(TACOS_E_CUDA, "synchronize: %s", cudaGetErrorString(cudaGetLastError()));
+      if (!r && seed_times) {
+        o.times.resize(pg.n_seeds);
+        combine_seed_times(pt, p->collective, pg.n_seeds, t_ag, t_rs, o.times.data());
       }
     }
+    if (tmp.p) device_pool().release(tmp.dev, tmp.p, tmp.cls);
+    pl.reset();
+    if (st) cudaStreamDestroy(st);
+    if (!go && !r) r = fail(TACOS_E_CUDA, "another device failed before the selection");
+    o.rc = r;
+    if (r) o.err = g_last_error;
+  };
+  {
+    std::vector<std::thread> th;
+    for (uint32_t g = 0; g < G; ++g) th.emplace_back(work, g);
+    for (auto &t : th) t.join();
+  }
+  cudaSetDevice(caller);
+  for (uint32_t g = 0; g < G; ++g)  // report a real failure before the knock-on ones
+    if (outs[g].rc && outs[g].err.find("another device failed") == std::string::npos)
+      return fail(outs[g].rc, "device %u: %s", g, outs[g].err.c_str());
+  for (uint32_t g = 0; g < G; ++g)
+    if (outs[g].rc) return fail(outs[g].rc, "device %u: %s", g, outs[g].err.c_str());
+  tacos_result res = outs[0].res;
+  res.visits = res.dest_events = res.matches = res.events = res.cancelled = res.n_sends = 0;
+  for (const ShardOut &o : outs) {
+    res.visits += o.res.visits;
+    res.dest_events += o.res.dest_events;
+    res.matches += o.res.matches;
+    res.events += o.res.events;
+    res.cancelled += o.res.cancelled;
+    res.n_sends += o.res.n_sends;
+  }
+  res.winner_local = (p->collective == TACOS_ALL_REDUCE) ? 3u : (coll_need_ag(p->collective) ? 1u : 2u);
+  *result = res;
+  if (seed_times) {
+    seed_times->clear();
+    for (const ShardOut &o : outs) seed_times->insert(seed_times->end(), o.times.begin(), o.times.end());
   }
   return TACOS_OK;
 }
@@ -1312,6 +1539,13 @@ extern "C" int tacos_synthesize_into(const tacos_topology *topo, const tacos_syn
                                      uint64_t capacity, tacos_result *result, void *stream) {
   if (!topo || !p || !result) return fail(TACOS_E_INVALID_ARG, "null argument");
   try {
+    uint32_t D = 1;
+    int rc = resolve_devices(p, &D);
+    if (rc) return rc;
+    if (D > 1) {  // seeds sharded over devices 0 .. D-1 (`stream` is not used: one stream per device)
+      if ((rc = validate_params(p))) return rc;
+      return synth_sharded(topo, p, D, sends, sends ? capacity : 0, result, nullptr);
+    }
     const tacos_topology *ts[1] = {topo};
     tacos_send *d[1] = {sends};
     uint64_t caps[1] = {sends ? capacity : 0};
@@ -1349,7 +1583,52 @@ extern "C" int tacos_synthesize_batch(const tacos_topology *const *topos, uint32
       caps[i] = n;
     }
     const bool keep = (p->flags & TACOS_FLAG_KEEP_SEED_TIMES) != 0;
-    rc = synth_many(topos, n_topos, p, dst.data(), caps.data(), res.data(), keep ? times.data() : nullptr, nullptr);
+    uint32_t D = 1;
+    if ((rc = resolve_devices(p, &D))) return rc;
+    if (D > 1 && n_topos == 1) {  // one topology: its seeds sharded over the devices
+      if ((rc = validate_params(p))) return rc;
+      rc = synth_sharded(topos[0], p, D, dst[0], caps[0], &res[0], keep ? &times[0] : nullptr);
+    } else if (D > 1) {  // topologies dealt round-robin to the devices, all seeds of one on one device
+      const uint32_t G = std::min(D, n_topos);
+      std::vector<int> rcs(G, 0);
+      std::vector<std::string> errs(G);
+      auto work = [&](uint32_t g) {
+        std::vector<const tacos_topology *> tg;
+        std::vector<tacos_send *> dg;
+        std::vector<uint64_t> cg;
+        std::vector<uint32_t> idx;
+        for (uint32_t i = g; i < n_topos; i += G) {
+          tg.push_back(topos[i]);
+          dg.push_back(dst[i]);
+          cg.push_back(caps[i]);
+          idx.push_back(i);
+        }
+        std::vector<tacos_result> rg(tg.size());
+        std::vector<std::vector<uint64_t>> tmg(tg.size());
+        tacos_synth_params pg = *p;
+        pg.n_devices = 1;
+        int r = cudaSetDevice((int)g) == cudaSuccess ? TACOS_OK : fail(TACOS_E_CUDA, "cudaSetDevice(%u)", g);
+        if (!r) r = synth_many(tg.data(), (uint32_t)tg.size(), &pg, dg.data(), cg.data(), rg.data(),
+                               keep ? tmg.data() : nullptr, nullptr);
+        if (!r)
+          for (size_t j = 0; j < idx.size(); ++j) {
+            res[idx[j]] = rg[j];
+            times[idx[j]] = std::move(tmg[j]);
+          }
+        rcs[g] = r;
+        if (r) errs[g] = g_last_error;
+      };
+      int caller = 0;
+      cudaGetDevice(&caller);
+      std::vector<std::thread> th;
+      for (uint32_t g = 0; g < G; ++g) th.emplace_back(work, g);
+      for (auto &t : th) t.join();
+      cudaSetDevice(caller);
+      for (uint32_t g = 0; g < G && !rc; ++g)
+        if (rcs[g]) rc = fail(rcs[g], "device %u: %s", g, errs[g].c_str());
+    } else {
+      rc = synth_many(topos, n_topos, p, dst.data(), caps.data(), res.data(), keep ? times.data() : nullptr, nullptr);
+    }
     if (rc) return rc;
     for (uint32_t i = 0; i < n_topos; ++i) {
       sch[i]->result = res[i];
@@ -1379,6 +1658,76 @@ extern "C" const uint64_t *tacos_schedule_seed_times(const tacos_schedule *s) {
   return s && !s->seed_times.empty() ? s->seed_times.data() : nullptr;
 }
 extern "C" void tacos_free_schedule(tacos_schedule *s) { delete s; }
+
+// ---------------------------------------------------------------------------
+// NCCL communicator of a multi-process job (one rank per GPU) and the exchange step
+// ---------------------------------------------------------------------------
+struct tacos_comm {
+  ncclComm_t comm = nullptr;
+  int device = -1;
+  const NcclApi *api = nullptr;
+};
+
+extern "C" int tacos_nccl_version(int32_t *version) {
+  if (!version) return fail(TACOS_E_INVALID_ARG, "null argument");
+  std::string err;
+  const NcclApi *api = nccl_api(&err);
+  if (!api) return fail(TACOS_E_NCCL, "%s", err.c_str());
+  int v = 0;
+  if (api->GetVersion(&v) != ncclSuccess) return fail(TACOS_E_NCCL, "ncclGetVersion failed");
+  *version = v;
+  return TACOS_OK;
+}
+
+extern "C" int tacos_comm_unique_id(uint8_t id[TACOS_COMM_ID_BYTES]) {
+  if (!id) return fail(TACOS_E_INVALID_ARG, "null argument");
+  static_assert(sizeof(ncclUniqueId) == TACOS_COMM_ID_BYTES, "NCCL unique id size");
+  std::string err;
+  const NcclApi *api = nccl_api(&err);
+  if (!api) return fail(TACOS_E_NCCL, "%s", err.c_str());
+  ncclUniqueId u;
+  const ncclResult_t r = api->GetUniqueId(&u);
+  if (r != ncclSuccess) return fail(TACOS_E_NCCL, "ncclGetUniqueId: %s", api->GetErrorString(r));
+  std::memcpy(id, &u, sizeof(u));
+  return TACOS_OK;
+}
+
+extern "C" int tacos_comm_init_rank(const uint8_t id[TACOS_COMM_ID_BYTES], int32_t n_ranks, int32_t rank,
+                                    tacos_comm **out) {
+  if (out) *out = nullptr;
+  if (!id || !out || n_ranks < 1 || rank < 0 || rank >= n_ranks) return fail(TACOS_E_INVALID_ARG, "bad argument");
+  int dev = -1, rc;
+  if ((rc = cuda_device_ok(&dev))) return rc;
+  std::string err;
+  const NcclApi *api = nccl_api(&err);
+  if (!api) return fail(TACOS_E_NCCL, "%s", err.c_str());
+  std::unique_ptr<tacos_comm> c(new (std::nothrow) tacos_comm());
+  if (!c) return fail(TACOS_E_NOMEM, "host allocation failed");
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  const ncclResult_t r = api->CommInitRank(&c->comm, n_ranks, u, rank);
+  if (r != ncclSuccess) return fail(TACOS_E_NCCL, "ncclCommInitRank: %s", api->GetErrorString(r));
+  c->device = dev;
+  c->api = api;
+  *out = c.release();
+  return TACOS_OK;
+}
+
+extern "C" void tacos_comm_destroy(tacos_comm *c) {
+  if (!c) return;
+  if (c->comm && c->api) c->api->CommDestroy(c->comm);
+  delete c;
+}
+
+extern "C" int tacos_plan_allreduce_keys(tacos_plan *pl, tacos_comm *c, void *stream) {
+  if (!pl || !c || !c->comm) return fail(TACOS_E_INVALID_ARG, "null argument");
+  if (pl->device != c->device)
+    return fail(TACOS_E_INVALID_ARG, "plan on device %d, communicator on device %d", pl->device, c->device);
+  uint64_t *keys = pl->parts[0].d_keys;
+  const ncclResult_t r = c->api->AllReduce(keys, keys, 2, ncclUint64, ncclMin, c->comm, (cudaStream_t)stream);
+  if (r != ncclSuccess) return fail(TACOS_E_NCCL, "ncclAllReduce: %s", c->api->GetErrorString(r));
+  return TACOS_OK;
+}
 
 // ---------------------------------------------------------------------------
 // tacos_eval: host replay ("a TEN link matched with a chunk";
