@@ -90,6 +90,12 @@ class tacos_winner(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
 
 
+class tacos_plan_info(ctypes.Structure):
+    _fields_ = [("n_jobs", ctypes.c_uint32), ("ctas", ctypes.c_uint32), ("cluster", ctypes.c_uint32),
+                ("threads", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32), ("rows_in_smem", ctypes.c_uint32),
+                ("links_in_smem", ctypes.c_uint32), ("launches", ctypes.c_uint32), ("rows_bytes", ctypes.c_uint64)]
+
+
 class tacos_cont_report(ctypes.Structure):
     _fields_ = [("T_ns", ctypes.c_double), ("T_rs_ns", ctypes.c_double), ("max_link_busy_ns", ctypes.c_double),
                 ("n_sends", ctypes.c_uint64)]
@@ -154,6 +160,7 @@ SIGNATURES = {
     "tacos_select_winner": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int32, ctypes.c_int,
                                            ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(tacos_winner)]),
     "tacos_plan_last_launches": (ctypes.c_uint32, [_VP]),
+    "tacos_plan_info_get": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_plan_info)]),
     "tacos_plan_stats": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_result), _VP]),
     "tacos_eval": (ctypes.c_int, [_VP, ctypes.POINTER(tacos_synth_params), _VP, ctypes.c_uint64,
                                   ctypes.POINTER(tacos_eval_report)]),
@@ -511,6 +518,11 @@ class Plan:
         _check(load_library().tacos_plan_stats(self.handle, ctypes.byref(res), ctypes.c_void_p(stream)),
                "tacos_plan_stats")
         return res.as_dict()
+
+    def info(self) -> dict:
+        inf = tacos_plan_info()
+        _check(load_library().tacos_plan_info_get(self.handle, ctypes.byref(inf)), "tacos_plan_info_get")
+        return {f: getattr(inf, f) for f, _ in inf._fields_}
 
     def last_launches(self) -> int:
         return int(load_library().tacos_plan_last_launches(self.handle))

@@ -1218,6 +1218,28 @@ extern "C" const uint64_t *tacos_plan_seed_times_device(const tacos_plan *pl, co
 
 extern "C" uint32_t tacos_plan_last_launches(const tacos_plan *pl) { return pl ? pl->last_launches : 0; }
 
+extern "C" int tacos_plan_info_get(const tacos_plan *pl, tacos_plan_info *out) {
+  if (!pl || !out) return fail(TACOS_E_INVALID_ARG, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  const Group *big = nullptr;
+  for (const Group &g : pl->groups) {
+    const uint32_t nj = g.job_end - g.job_begin, q = g.lay.cluster ? g.lay.cluster : 1u;
+    out->n_jobs += nj;
+    out->ctas += nj * q;
+    out->launches += 1;
+    if (!g.lay.rows_in_smem) out->rows_bytes += (uint64_t)nj * g.lay.rows_bytes;
+    if (!big || nj > big->job_end - big->job_begin) big = &g;
+  }
+  if (big) {
+    out->cluster = big->lay.cluster ? big->lay.cluster : 1u;
+    out->threads = big->lay.threads;
+    out->smem_bytes = big->lay.smem_bytes;
+    out->rows_in_smem = big->lay.rows_in_smem;
+    out->links_in_smem = big->lay.links_in_smem;
+  }
+  return TACOS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // one-call synthesis
 // ---------------------------------------------------------------------------

@@ -1,6 +1,6 @@
 """Summarize ncu outputs from gpurun_out/ into profiles/ (committed evidence).
 
-usage: python tools/make_profiles.py ROUND_TAG WORKLOAD launches.csv report.ncu-rep
+usage: python tools/make_profiles.py ROUND_TAG WORKLOAD launches.csv|- report.ncu-rep
 Writes:
   profiles/<tag>_launches_<workload>.csv   per-kernel totals of the launch list (share of the step)
   profiles/<tag>_ncu_<workload>.txt        key metrics + per-line stall summary of the top kernel
@@ -52,12 +52,13 @@ def num(x):
 def main():
     tag, workload, lcsv, rep = sys.argv[1:5]
     os.makedirs(PROF, exist_ok=True)
-    agg = launches(lcsv)
-    tot = sum(sum(v) for v in agg.values())
-    with open(os.path.join(PROF, f"{tag}_launches_{workload}.csv"), "w") as fh:
-        fh.write("kernel,launches,total_us,avg_us,share\n")
-        for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-            fh.write(f"{k},{len(v)},{sum(v):.1f},{sum(v) / len(v):.2f},{sum(v) / tot:.4f}\n")
+    if lcsv != "-":
+        agg = launches(lcsv)
+        tot = sum(sum(v) for v in agg.values())
+        with open(os.path.join(PROF, f"{tag}_launches_{workload}.csv"), "w") as fh:
+            fh.write("kernel,launches,total_us,avg_us,share\n")
+            for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+                fh.write(f"{k},{len(v)},{sum(v):.1f},{sum(v) / len(v):.2f},{sum(v) / tot:.4f}\n")
     mets = raw_metrics(rep)
     lines = []
     traffic = None
@@ -67,7 +68,9 @@ def main():
             "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__block_size",
             "launch__grid_size", "launch__cluster_dim_x", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__cycles_active.avg",
-            "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
+            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg",
+            "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors.sum"]
+    extra = {}
     for m in mets:
         name = m.get("Kernel Name", ("?", ""))[0]
         lines.append(f"kernel: {name}")
@@ -80,6 +83,13 @@ def main():
             rv, ru = m.get("dram__bytes_read.sum", ("nan", "byte"))
             wv, wu = m.get("dram__bytes_write.sum", ("nan", "byte"))
             traffic = num(rv) * scale.get(ru, 1) + num(wv) * scale.get(wu, 1)
+            wf = num(m.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", ("nan", ""))[0])
+            cyc = num(m.get("sm__cycles_elapsed.avg", ("nan", ""))[0])
+            n_sm = 148
+            extra = {"smem_pipe_frac": wf / (cyc * n_sm) if cyc == cyc and wf == wf else None,
+                     "issue_active_pct": num(m.get("smsp__issue_active.avg.pct_of_peak_sustained_active", ("nan", ""))[0]),
+                     "warps_active_pct": num(m.get("sm__warps_active.avg.pct_of_peak_sustained_active", ("nan", ""))[0]),
+                     "kernel_ms": num(m.get("gpu__time_duration.sum", ("nan", ""))[0])}
     src = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), rep, "25"], capture_output=True,
                          text=True).stdout
     with open(os.path.join(PROF, f"{tag}_ncu_{workload}.txt"), "w") as fh:
@@ -88,9 +98,11 @@ def main():
     tj = os.path.join(PROF, "ncu_traffic.json")
     data = json.load(open(tj)) if os.path.exists(tj) else {}
     if traffic is not None:
-        data[workload] = {"kernel": "greedy_kernel", "dram_bytes_per_launch": traffic, "source": f"{tag}_ncu_{workload}.txt"}
+        data[workload] = dict({"kernel": "greedy_kernel", "dram_bytes_per_launch": traffic,
+                               "source": f"{tag}_ncu_{workload}.txt"}, **extra)
     json.dump(data, open(tj, "w"), indent=1)
-    print(open(os.path.join(PROF, f"{tag}_launches_{workload}.csv")).read())
+    if lcsv != "-":
+        print(open(os.path.join(PROF, f"{tag}_launches_{workload}.csv")).read())
     print("\n".join(lines))
     print("traffic", traffic)
 
