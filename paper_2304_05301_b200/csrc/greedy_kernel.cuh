@@ -150,6 +150,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const uint32_t d_lo = min(N, crank * chunkN), d_hi = min(N, d_lo + chunkN);
   const uint32_t p_lo = __ldg(&in_ptr[d_lo]), p_hi = __ldg(&in_ptr[d_hi]);
   const bool worklist = lay.worklist != 0u;
+  TCHECK(lay.smem_bytes <= dynamic_smem_bytes(), "layout exceeds the dynamic shared memory");
+  TCHECK(d_lo <= d_hi && p_lo <= p_hi && p_hi <= L, "CTA ranges");
   auto cluster_barrier = [&]() {
     if (Q > 1) cluster.sync();
     else __syncthreads();
@@ -268,6 +270,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         rc.chunk = rch[2u * q + par];
         rc.link = lid;
         rc.t_start = t_start;
+        TCHECK(base + wpre[wi] + __popc(word & (bit - 1u)) < job.rec_cap && q >= p_lo && q < p_hi, "send record");
         rec[base + wpre[wi] + __popc(word & (bit - 1u))] = rc;
       }
     }
@@ -340,6 +343,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         for (int u = 0; u < kPA; ++u) {
           if (!arrq[u]) continue;
           const uint32_t q = qb + (uint32_t)u * nthr, c = cq[u], d = dq[u];
+          TCHECK(d < N && c < T.C && q >= p_lo && q < p_hi, "arrival");
           atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
           hver[d] = e;
           cur[q] = kNone;
@@ -430,6 +434,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         uint32_t base = 0;
         if (lane == 0 && bal) base = atomicAdd(&s_nwork, (uint32_t)__popc(bal));
         base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        TCHECK(!active || base + __popc(bal & ((1u << lane) - 1u)) < d_hi - d_lo, "worklist");
         if (active) s_list[base + __popc(bal & ((1u << lane) - 1u))] = d_lo + i;
       }
       myV += nfree;
@@ -457,6 +462,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         const uint32_t d = worklist ? s_list[wi] : d_lo + wi;
         const uint32_t b0 = s_inptr[d], b1 = s_inptr[d + 1];
         const uint32_t deg = b1 - b0;
+        TCHECK(d >= d_lo && d < d_hi && b0 >= p_lo && b1 <= p_hi && b0 <= b1, "destination range");
         uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
         uint4 hv[V];
 
@@ -464,6 +470,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         // held[src] row of in-link p into registers (own shared memory, a peer's via DSMEM, or L2)
         auto load_row = [&](uint32_t p, uint4 (&cv)[V]) {
           const uint32_t sp = t_src[p];
+          TCHECK(sp < N && p >= p_lo && p < p_hi, "walk row");
           // Row chunk order is vector-major: vector v of lane gl holds words (v*P + gl)*4 .. +3.
           const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
           if (!ROWS_SMEM) {  // rows in HBM/L2, written by other SMs of the cluster: L2-coherent loads
@@ -543,6 +550,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
           uint32_t chunk = (((uint32_t)vsel * P + gl) * 4u + wi) * 32u + bit;
           if (P > 1) chunk = __shfl_sync(gmask, chunk, __ffs(__ballot_sync(gmask, mine)) - 1);
+          TCHECK(chunk < T.C && t_lid[p] < L, "claimed chunk");
           if (gl == 0) {
             cur[p] = chunk;
             rch[2u * p + (e & 1u)] = (uint16_t)chunk;
@@ -823,6 +831,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             }
             if (mine) {  // claim (R4): the owning lane writes the link
               const uint32_t chunk = ((((uint32_t)(gl * V) + (uint32_t)vsel) * 4u + wi) * 32u) + bit;
+              TCHECK(chunk < T.C && pp >= p_lo && pp < p_hi, "claimed chunk (lane pair)");
               cur[pp] = chunk;
               rch[2u * pp + (e & 1u)] = (uint16_t)chunk;
               const uint32_t wp = t_w[pp];

@@ -122,6 +122,7 @@ literal_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const La
               r.chunk = c;
               r.link = __ldg(&p_lid[p]);
               r.t_start = t - __ldg(&p_w[p]);
+              TCHECK(idx < job.rec_cap && c < T.C, "literal record");
               rec[idx] = r;
             }
           }

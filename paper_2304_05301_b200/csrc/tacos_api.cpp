@@ -23,6 +23,7 @@
 #include <new>
 #include <string>
 #include <unordered_map>
+#include <tuple>
 #include <unordered_set>
 #include <vector>
 
@@ -502,6 +503,7 @@ struct tacos_plan {
   size_t sort_bytes = 0;
   uint64_t *h_small = nullptr;  // pinned: per part {keys[2], stats[5]}
   DevBuf h_small_buf;
+  DevBuf stage_buf;             // pinned staging block of the plan's one H2D upload
   std::vector<DevBuf> bufs;
   uint32_t last_launches = 0;
   unsigned long long *d_trace = nullptr;
@@ -516,6 +518,7 @@ struct tacos_plan {
     }
     for (auto &b : bufs) device_pool().release(b.dev, b.p, b.cls);
     if (h_small_buf.p) pinned_pool().release(h_small_buf.dev, h_small_buf.p, h_small_buf.cls);
+    if (stage_buf.p) pinned_pool().release(stage_buf.dev, stage_buf.p, stage_buf.cls);
   }
 };
 
@@ -671,7 +674,58 @@ uint32_t pow2_at_least(uint32_t x) {
   return p;
 }
 
-int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p, tacos_plan **out) {
+// st: the stream the plan's first search will run on; the one staged upload of the plan's
+// host-built arrays is ordered on it (no synchronization).  nullptr: upload on the legacy
+// stream and synchronize (tacos_plan_create, whose caller's stream is not known yet).
+// Cluster size chosen for a launch shape (per device), so repeated syntheses skip the
+// occupancy queries.
+struct ClusterKey {
+  int dev;
+  uint32_t N, L, W, P, V, jobs, reg_path, masked, worklist, smem;
+  bool operator<(const ClusterKey &o) const {
+    return std::tie(dev, N, L, W, P, V, jobs, reg_path, masked, worklist, smem) <
+           std::tie(o.dev, o.N, o.L, o.W, o.P, o.V, o.jobs, o.reg_path, o.masked, o.worklist, o.smem);
+  }
+};
+std::mutex g_cluster_mu;
+std::map<ClusterKey, uint32_t> &cluster_cache() {
+  static auto *m = new std::map<ClusterKey, uint32_t>();
+  return *m;
+}
+bool cluster_cache_get(const ClusterKey &k, uint32_t *q) {
+  std::lock_guard<std::mutex> g(g_cluster_mu);
+  auto it = cluster_cache().find(k);
+  if (it == cluster_cache().end()) return false;
+  *q = it->second;
+  return true;
+}
+void cluster_cache_put(const ClusterKey &k, uint32_t q) {
+  std::lock_guard<std::mutex> g(g_cluster_mu);
+  cluster_cache()[k] = q;
+}
+
+// Host-built arrays of a plan, staged into one host buffer and shipped with one H2D copy
+// into one device block: reserve() / add() return byte offsets; device addresses are
+// base + offset once the block exists (structs holding device pointers are written into
+// their reserved slots after that).
+struct PlanStage {
+  std::vector<unsigned char> host;
+  size_t add(const void *src, size_t n) {
+    const size_t off = reserve(n);
+    if (n) std::memcpy(host.data() + off, src, n);
+    return off;
+  }
+  size_t reserve(size_t n) {
+    const size_t off = (host.size() + 255) / 256 * 256;
+    host.resize(off + n + 16, 0);
+    return off;
+  }
+  template <typename T>
+  void put(size_t off, const T &v) { std::memcpy(host.data() + off, &v, sizeof(T)); }
+};
+
+int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p, tacos_plan **out,
+               cudaStream_t st = nullptr, bool sync = true) {
   *out = nullptr;
   int rc = validate_params(p);
   if (rc) return rc;
@@ -819,7 +873,19 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     // occupancy calculator for the kernel this layout selects: only 15 clusters of 8 fit on a
     // B200, so config 4's 16 jobs take Q = 6, 579 ms vs 625 ms at Q = 4; waves of clusters
     // would double the time). TACOS_CLUSTER overrides.
-    if (!(p->flags & TACOS_FLAG_LITERAL) && !getenv("TACOS_CLUSTER")) {
+    // (the choice is cached per shape: the occupancy queries cost more than a small synthesis)
+    const ClusterKey ck{dev, maxN, maxL, maxW, P0, V0, n_jobs - begin, g.lay.reg_path, g.lay.masked, g.lay.worklist,
+                        (uint32_t)smem_limit};
+    uint32_t cached_q = 0;
+    if (!(p->flags & TACOS_FLAG_LITERAL) && !getenv("TACOS_CLUSTER") && cluster_cache_get(ck, &cached_q)) {
+      if (cached_q != g.lay.cluster) {
+        Layout lq = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, n_jobs - begin, (uint32_t)n_sms, cached_q);
+        lq.reg_path = g.lay.reg_path;
+        lq.masked = g.lay.masked;
+        lq.worklist = g.lay.worklist;
+        g.lay = lq;
+      }
+    } else if (!(p->flags & TACOS_FLAG_LITERAL) && !getenv("TACOS_CLUSTER")) {
       const uint32_t jobs = n_jobs - begin;
       for (uint32_t q = 8; q > g.lay.cluster; --q) {
         if ((uint64_t)jobs * q > (uint64_t)n_sms || maxN / q < 64u) continue;
@@ -836,6 +902,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
           break;
         }
       }
+      cluster_cache_put(ck, g.lay.cluster);
     }
     if ((size_t)g.lay.smem_bytes > smem_limit)  // the per-NPU / per-link arrays that always stay on chip
       return fail(TACOS_E_OVERFLOW, "search state needs %u B of shared memory per CTA (limit %zu)", g.lay.smem_bytes,
@@ -846,7 +913,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     gi = gj;
   }
 
-  // ---- device allocations ----
+  // ---- device memory: big scratch blocks, then one staged block for everything host-built ----
   auto &bufs = pl->bufs;
   void *vp = nullptr;
   size_t rows_total = 0, links_total = 0;
@@ -863,28 +930,40 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     if ((rc = dev_alloc(bufs, dev, links_total, &vp))) return rc;
     pl->d_links = reinterpret_cast<unsigned char *>(vp);
   }
-  if ((rc = dev_alloc(bufs, dev, sizeof(JobOut) * n_jobs, &vp))) return rc;
-  pl->d_outs = reinterpret_cast<JobOut *>(vp);
-  if ((rc = dev_alloc(bufs, dev, 8, &vp))) return rc;
-  pl->d_count = reinterpret_cast<unsigned long long *>(vp);
   uint64_t max_M = 0;
   for (uint32_t i = 0; i < n_topos; ++i) {
     Part &pt = pl->parts[i];
-    const tacos_topology *t = pt.topo;
-    if ((rc = upload(bufs, dev, pt.w.data(), pt.w.size(), &pt.d_w))) return rc;
-    // per-position costs for both orientations
-    uint32_t *d_pos_w[2];
-    for (int o = 0; o < 2; ++o) {
-      std::vector<uint32_t> pw(pt.L);
-      for (uint32_t q = 0; q < pt.L; ++q) pw[q] = pt.w[t->pos_lid[o][q]];
-      if ((rc = upload(bufs, dev, pw.data(), pw.size(), &d_pos_w[o]))) return rc;
+    if (record) {
+      if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.cap * pt.n_jobs, &vp))) return rc;
+      pt.d_rec = reinterpret_cast<Rec *>(vp);
     }
-    uint32_t *d_pre = nullptr, *d_post = nullptr, *d_allow[2] = {nullptr, nullptr};
+    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL)) && record) max_M = std::max(max_M, pt.cap);
+  }
+  if (max_M) {
+    pl->sort_bytes = rs_sort_scratch_bytes(max_M);
+    if ((rc = dev_alloc(bufs, dev, pl->sort_bytes, &pl->d_sort))) return rc;
+  }
+  PlanStage sg;
+  const size_t o_outs = sg.reserve(sizeof(JobOut) * n_jobs), o_count = sg.reserve(8);
+  struct PartOffs {
+    size_t w, pos_w[2], allow[2] = {0, 0}, pre = 0, post = 0, topo[2], keys, times_ag, times_rs = 0;
+  };
+  std::vector<PartOffs> po(n_topos);
+  for (uint32_t i = 0; i < n_topos; ++i) {
+    Part &pt = pl->parts[i];
+    const tacos_topology *t = pt.topo;
+    PartOffs &o = po[i];
+    o.w = sg.add(pt.w.data(), pt.w.size() * 4);
+    for (int q = 0; q < 2; ++q) {  // per-position costs of both orientations
+      std::vector<uint32_t> pw(pt.L);
+      for (uint32_t x = 0; x < pt.L; ++x) pw[x] = pt.w[t->pos_lid[q][x]];
+      o.pos_w[q] = sg.add(pw.data(), pw.size() * 4);
+    }
     if (relay) {
-      for (int o = 0; o < 2; ++o) {
+      for (int q = 0; q < 2; ++q) {
         std::vector<uint32_t> allow;
-        relay_allow(t, o, pt.C, pt.Wp, pl->pre, pl->post, allow);
-        if ((rc = upload(bufs, dev, allow.data(), allow.size(), &d_allow[o]))) return rc;
+        relay_allow(t, q, pt.C, pt.Wp, pl->pre, pl->post, allow);
+        o.allow[q] = sg.add(allow.data(), allow.size() * 4);
       }
     }
     if (custom) {
@@ -895,11 +974,25 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
           pre_p[(size_t)x * pt.Wp + q] = pl->pre[(size_t)x * W0 + q];
           post_p[(size_t)x * pt.Wp + q] = pl->post[(size_t)x * W0 + q];
         }
-      if ((rc = upload(bufs, dev, pre_p.data(), pre_p.size(), &d_pre))) return rc;
-      if ((rc = upload(bufs, dev, post_p.data(), post_p.size(), &d_post))) return rc;
+      o.pre = sg.add(pre_p.data(), pre_p.size() * 4);
+      o.post = sg.add(post_p.data(), post_p.size() * 4);
     }
-    for (int o = 0; o < 2; ++o) {
-      DevTopo &h = pt.htopo[o];
+    for (int q = 0; q < 2; ++q) o.topo[q] = sg.reserve(sizeof(DevTopo));
+    o.keys = sg.reserve(8 * 8);
+    o.times_ag = sg.reserve(8 * (size_t)S);
+    if (pt.rs_search) o.times_rs = sg.reserve(8 * (size_t)S);
+  }
+  const size_t o_jobs = sg.reserve(sizeof(Job) * n_jobs);
+  if ((rc = dev_alloc(bufs, dev, sg.host.size(), &vp))) return rc;
+  unsigned char *base = reinterpret_cast<unsigned char *>(vp);
+  pl->d_outs = reinterpret_cast<JobOut *>(base + o_outs);
+  pl->d_count = reinterpret_cast<unsigned long long *>(base + o_count);
+  for (uint32_t i = 0; i < n_topos; ++i) {
+    Part &pt = pl->parts[i];
+    const PartOffs &o = po[i];
+    pt.d_w = reinterpret_cast<uint32_t *>(base + o.w);
+    for (int q = 0; q < 2; ++q) {
+      DevTopo &h = pt.htopo[q];
       h.N = pt.N;
       h.L = pt.L;
       h.C = pt.C;
@@ -909,34 +1002,21 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       h.VPL = pt.VPL;
       h.custom = custom ? 1u : 0u;
       h.required = pt.required;
-      h.in_ptr = pt.td->d_in_ptr[o];
-      h.p_src = pt.td->d_pos_src[o];
-      h.p_dst = pt.td->d_pos_dst[o];
-      h.p_w = d_pos_w[o];
-      h.p_lid = pt.td->d_pos_lid[o];
-      h.pre = d_pre;
-      h.post = d_post;
-      h.allow = d_allow[o];
-      if ((rc = upload(bufs, dev, &h, 1, &pt.d_topo[o]))) return rc;
+      h.in_ptr = pt.td->d_in_ptr[q];
+      h.p_src = pt.td->d_pos_src[q];
+      h.p_dst = pt.td->d_pos_dst[q];
+      h.p_w = reinterpret_cast<const uint32_t *>(base + o.pos_w[q]);
+      h.p_lid = pt.td->d_pos_lid[q];
+      h.pre = custom ? reinterpret_cast<const uint32_t *>(base + o.pre) : nullptr;
+      h.post = custom ? reinterpret_cast<const uint32_t *>(base + o.post) : nullptr;
+      h.allow = relay ? reinterpret_cast<const uint32_t *>(base + o.allow[q]) : nullptr;
+      sg.put(o.topo[q], h);
+      pt.d_topo[q] = reinterpret_cast<DevTopo *>(base + o.topo[q]);
     }
-    if (record) {
-      if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.cap * pt.n_jobs, &vp))) return rc;
-      pt.d_rec = reinterpret_cast<Rec *>(vp);
-    }
-    if ((rc = dev_alloc(bufs, dev, 8 * 8, &vp))) return rc;
-    pt.d_keys = reinterpret_cast<uint64_t *>(vp);
+    pt.d_keys = reinterpret_cast<uint64_t *>(base + o.keys);
     pt.d_stats = pt.d_keys + 2;
-    if ((rc = dev_alloc(bufs, dev, 8 * (size_t)S, &vp))) return rc;
-    pt.d_times_ag = reinterpret_cast<uint64_t *>(vp);
-    if (pt.rs_search) {
-      if ((rc = dev_alloc(bufs, dev, 8 * (size_t)S, &vp))) return rc;
-      pt.d_times_rs = reinterpret_cast<uint64_t *>(vp);
-    }
-    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL)) && record) max_M = std::max(max_M, pt.cap);
-  }
-  if (max_M) {
-    pl->sort_bytes = rs_sort_scratch_bytes(max_M);
-    if ((rc = dev_alloc(bufs, dev, pl->sort_bytes, &pl->d_sort))) return rc;
+    pt.d_times_ag = reinterpret_cast<uint64_t *>(base + o.times_ag);
+    if (pt.rs_search) pt.d_times_rs = reinterpret_cast<uint64_t *>(base + o.times_rs);
   }
   // ---- job table ----
   pl->jobs.resize(n_jobs);
@@ -954,6 +1034,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         jb.sigma = sigma;
         jb.out_slot = pt.job_base + j;
         jb.rec = record ? pt.d_rec + (size_t)j * pt.cap : nullptr;
+        jb.rec_cap = record ? pt.cap : 0;
         jb.g_rows = nullptr;
         jb.g_links = nullptr;
         jb.trace = nullptr;
@@ -971,19 +1052,28 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   }
   if (getenv("TACOS_TRACE") && !pl->jobs.empty()) {
     if ((rc = dev_alloc(bufs, dev, 8ull * kTraceWords * kTraceEvents * 8, &vp))) return rc;
-    CUDA_TRY(cudaMemset(vp, 0xFF, 8ull * kTraceWords * kTraceEvents * 8));
+    CUDA_TRY(cudaMemsetAsync(vp, 0xFF, 8ull * kTraceWords * kTraceEvents * 8, st));
     pl->jobs[0].trace = reinterpret_cast<unsigned long long *>(vp);
     pl->jobs[0].trace_stride = 1u;
     if (const char *env = getenv("TACOS_TRACE_STRIDE")) pl->jobs[0].trace_stride = std::max(1, atoi(env));
     pl->d_trace = pl->jobs[0].trace;
   }
-  if ((rc = upload(bufs, dev, pl->jobs.data(), pl->jobs.size(), &pl->d_jobs))) return rc;
+  std::memcpy(sg.host.data() + o_jobs, pl->jobs.data(), sizeof(Job) * n_jobs);
+  pl->d_jobs = reinterpret_cast<Job *>(base + o_jobs);
+  // one pinned staging copy + one H2D on `st`; the pinned block stays with the plan (released
+  // after its last work completes), so nothing here waits for the copy
+  pl->stage_buf.dev = dev;
+  pl->stage_buf.p = pinned_pool().alloc(dev, sg.host.size(), &pl->stage_buf.cls);
+  if (!pl->stage_buf.p) return fail(TACOS_E_NOMEM, "pinned allocation failed");
+  std::memcpy(pl->stage_buf.p, sg.host.data(), sg.host.size());
+  CUDA_TRY(cudaEventCreateWithFlags(&pl->done, cudaEventDisableTiming));
+  CUDA_TRY(cudaMemcpyAsync(base, pl->stage_buf.p, sg.host.size(), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(pl->done, st));
   pl->h_small_buf.dev = dev;
   pl->h_small_buf.p = pinned_pool().alloc(dev, 8 * 8 * (size_t)n_topos, &pl->h_small_buf.cls);
   if (!pl->h_small_buf.p) return fail(TACOS_E_NOMEM, "pinned allocation failed");
   pl->h_small = reinterpret_cast<uint64_t *>(pl->h_small_buf.p);
-  CUDA_TRY(cudaEventCreateWithFlags(&pl->done, cudaEventDisableTiming));
-  CUDA_TRY(cudaStreamSynchronize(nullptr));
+  if (sync) CUDA_TRY(cudaStreamSynchronize(st));
   *out = pl.release();
   return TACOS_OK;
 }
@@ -1324,7 +1414,7 @@ int read_seed_times_async(const Part &pt, uint32_t S, std::vector<uint64_t> &t_a
 int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p, tacos_send **dst,
                const uint64_t *caps, tacos_result *results, std::vector<uint64_t> *seed_times, cudaStream_t st) {
   tacos_plan *raw = nullptr;
-  int rc = plan_build(topos, n_topos, p, &raw);
+  int rc = plan_build(topos, n_topos, p, &raw, st, false);
   if (rc) return rc;
   std::unique_ptr<tacos_plan> pl(raw);
   if ((rc = plan_search(pl.get(), st))) return rc;
@@ -1476,7 +1566,7 @@ int synth_sharded(const tacos_topology *topo, const tacos_synth_params *p, uint3
     pg.n_seeds = hi - lo;
     if (cudaSetDevice((int)g) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
       r = fail(TACOS_E_CUDA, "device %u: %s", g, cudaGetErrorString(cudaGetLastError()));
-    if (!r) r = plan_build(&topo, 1, &pg, &raw);
+    if (!r) r = plan_build(&topo, 1, &pg, &raw, st, false);
     std::unique_ptr<tacos_plan> pl(raw);
     if (!r) r = plan_search(pl.get(), st);
     const bool go = rv.arrive(r != 0);

@@ -17,6 +17,33 @@ int check_launch(const char *what);
 // Philox4x32-10 (R2; Salmon et al. SC'11).  Counter (t_lo, t_hi, link, sigma),
 // key (seed_lo, seed_hi); word 0 = order key, word 1 = pick draw.
 // ---------------------------------------------------------------------------
+// Bounds-checked build (build.py --variant checked -DTACOS_CHECKED=1, loaded through
+// TACOS_LIB): every shared-memory / global index of the search kernels is checked and a
+// violation traps with its site.  Stands in for compute-sanitizer, which is closed on the
+// GPU pool.
+#ifndef TACOS_CHECKED
+#define TACOS_CHECKED 0
+#endif
+#if TACOS_CHECKED
+#define TCHECK(cond, what)                                                                              \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("tacos check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                              \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define TCHECK(cond, what) \
+  do {                     \
+  } while (0)
+#endif
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+  uint32_t r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {

@@ -47,6 +47,7 @@ struct Job {
   uint32_t sigma;
   uint32_t out_slot;
   Rec *rec;              // nullptr: recording off
+  uint64_t rec_cap;      // records the job may write (bounds-checked build)
   uint32_t *g_rows;      // global rows (held | have) when they do not fit in smem
   unsigned char *g_links;// global per-position arrays when they do not fit in smem
   unsigned long long *trace;  // debug (TACOS_TRACE): per CTA rank, per event {t, delivered, local min, matches}
