@@ -50,6 +50,9 @@ constexpr bool kP1Smem = true;
 #define TACOS_P1_HAVE_REG 0
 #endif
 
+#ifndef TACOS_STEP1  // 1: the P == 1 walk step keeps per-word counts and selects the bit without POPC
+#define TACOS_STEP1 1  // measured: config 2 0.283 -> 0.269 ms, config 3 0.745 -> 0.740, config 5 3.044 -> 3.015
+#endif
 #ifndef TACOS_MIN_BLOCKS  // resident CTAs per SM the register budget is sized for
 #define TACOS_MIN_BLOCKS 1
 #endif
@@ -156,6 +159,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     if (Q > 1) cluster.sync();
     else __syncthreads();
   };
+
   // owner CTA of NPU x = x / chunkN, by a multiply-high with m = ceil(2^32 / chunkN):
   // exact while x * (m * chunkN - 2^32) < 2^32, i.e. for N < 2^16
   // (chunkN = 1 would need m = 2^32: the owner is x itself)
@@ -481,8 +485,94 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             for (int v = 0; v < V; ++v) cv[v] = h4[v * P + gl];
           }
         };
+        // One lane per destination (P == 1): the per-word counts of the candidate row are kept
+        // for the selection (vector -> word -> bit), and the bit select runs without POPC.
+        auto step_row1 = [&](uint32_t p, uint32_t pk, uint4 (&cv)[V]) {
+          uint32_t wd[4 * V], pc[4 * V], vt[V];
+          uint32_t K = 0;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if constexpr (kHaveSmem) cv[v] = andnot4(cv[v], have4[v]);  // held[src] & ~have[d]
+            else cv[v] = andnot4(cv[v], hv[v]);
+            if constexpr (MASKED)  // & allow[p]: post[d] plus the relays of this link
+              cv[v] = and4(cv[v], __ldg(reinterpret_cast<const uint4 *>(T.allow + (size_t)p * Wp) + v));
+            wd[4 * v + 0] = cv[v].x;
+            wd[4 * v + 1] = cv[v].y;
+            wd[4 * v + 2] = cv[v].z;
+            wd[4 * v + 3] = cv[v].w;
+          }
+#pragma unroll
+          for (int i = 0; i < 4 * V; ++i) pc[i] = __popc(wd[i]);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            vt[v] = (pc[4 * v] + pc[4 * v + 1]) + (pc[4 * v + 2] + pc[4 * v + 3]);
+            K += vt[v];
+          }
+          if (K == 0u) {
+            seen[p] = hver_of(t_src[p]);
+            return;
+          }
+          uint32_t rv = __umulhi(pk, K);  // floor(u_pick * K / 2^32)
+          uint32_t vsel = 0;
+#pragma unroll
+          for (int v = 0; v + 1 < V; ++v) {
+            const bool adv = (vsel == (uint32_t)v) && (rv >= vt[v]);
+            rv = adv ? rv - vt[v] : rv;
+            vsel = adv ? (uint32_t)v + 1u : vsel;
+          }
+          uint32_t q0 = pc[0], q1 = pc[1], q2 = pc[2];
+          uint4 x = cv[0];
+#pragma unroll
+          for (int v = 1; v < V; ++v) {
+            const bool m = vsel == (uint32_t)v;
+            q0 = m ? pc[4 * v] : q0;
+            q1 = m ? pc[4 * v + 1] : q1;
+            q2 = m ? pc[4 * v + 2] : q2;
+            x = m ? cv[v] : x;
+          }
+          uint32_t wi = 0, word = x.x;
+          bool m = rv >= q0;
+          rv = m ? rv - q0 : rv; wi = m ? 1u : wi; word = m ? x.y : word;
+          m = m && rv >= q1;
+          rv = m ? rv - q1 : rv; wi = m ? 2u : wi; word = m ? x.z : word;
+          m = m && rv >= q2;
+          rv = m ? rv - q2 : rv; wi = m ? 3u : wi; word = m ? x.w : word;
+          const uint32_t bit = select_bit_swar(word, rv);
+          const uint32_t mask = 1u << bit;
+          // claim: withheld from d's other in-links (R4)
+          if constexpr (kHaveSmem) {
+            reinterpret_cast<uint32_t *>(have4)[vsel * 4u + wi] |= mask;  // one word, dynamic index
+          } else {
+            const uint32_t sel = vsel * 4u + wi;  // flat word index: independent predicated ORs
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              hv[v].x |= sel == (uint32_t)(4 * v + 0) ? mask : 0u;
+              hv[v].y |= sel == (uint32_t)(4 * v + 1) ? mask : 0u;
+              hv[v].z |= sel == (uint32_t)(4 * v + 2) ? mask : 0u;
+              hv[v].w |= sel == (uint32_t)(4 * v + 3) ? mask : 0u;
+            }
+          }
+          const uint32_t chunk = (vsel * 4u + wi) * 32u + bit;
+          TCHECK(chunk < T.C && t_lid[p] < L, "claimed chunk");
+          cur[p] = chunk;
+          rch[2u * p + (e & 1u)] = (uint16_t)chunk;
+          const uint32_t wp = t_w[p];
+          busy[p] = t + wp;
+          mo_w = wp < mo_w ? wp : mo_w;
+          ++myM;
+          ++my_claims;
+          const uint32_t lid = t_lid[p];
+          atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
+        };
+
         // One step of the matching walk (a5) on in-link p, pick draw pk, loaded row cv.
         auto step_row = [&](uint32_t p, uint32_t pk, uint4 (&cv)[V]) {
+#if TACOS_STEP1
+          if constexpr (P == 1) {
+            step_row1(p, pk, cv);
+            return;
+          }
+#endif
           uint32_t incl[V], tot[V];
           uint32_t K = 0;
 #pragma unroll

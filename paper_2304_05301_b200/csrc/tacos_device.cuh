@@ -69,6 +69,27 @@ __device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t r) {
   return pos;
 }
 
+// Same result without POPC (POPC issues on the XU pipe at a fraction of the ALU rate):
+// SWAR bit counts of the 2-bit pairs, nibbles and bytes, the inclusive byte prefix by one
+// multiply, then byte -> nibble -> pair -> bit, all on the ALU / FMA pipes.
+__device__ __forceinline__ uint32_t select_bit_swar(uint32_t x, uint32_t r) {
+  const uint32_t c1 = x - ((x >> 1) & 0x55555555u);                    // 2-bit counts
+  const uint32_t c2 = (c1 & 0x33333333u) + ((c1 >> 2) & 0x33333333u);  // 4-bit counts
+  const uint32_t c3 = (c2 + (c2 >> 4)) & 0x0F0F0F0Fu;                  // byte counts
+  const uint32_t pre = c3 * 0x01010101u;  // byte i: set bits in bytes 0..i (monotone)
+  const uint32_t p0 = pre & 0xFFu, p1 = (pre >> 8) & 0xFFu, p2 = (pre >> 16) & 0xFFu;
+  uint32_t pos = 0, base = 0;
+  if (r >= p0) { pos = 8u; base = p0; }
+  if (r >= p1) { pos = 16u; base = p1; }
+  if (r >= p2) { pos = 24u; base = p2; }
+  r -= base;
+  const uint32_t n = (c2 >> pos) & 0xFu;
+  if (r >= n) { r -= n; pos += 4u; }
+  const uint32_t q = (c1 >> pos) & 0x3u;
+  if (r >= q) { r -= q; pos += 2u; }
+  return pos + ((r >= ((x >> pos) & 1u)) ? 1u : 0u);
+}
+
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) { return __reduce_add_sync(0xFFFFFFFFu, v); }
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
 #pragma unroll
