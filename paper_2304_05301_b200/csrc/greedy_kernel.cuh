@@ -313,6 +313,415 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     draw_ahead(0ull, tid, nthr);
   }
 
+  // ========================================================================================
+  // Windowed event loop (lay.window = W > 0; wide rows on the register path, several link
+  // costs, no relays).  Every arrival inside [T0, T0 + W), W <= the smallest link cost, comes
+  // from a send that started before T0: a send started at t >= T0 ends at t + w >= T0 + W.
+  // So at the window start T0 every event time of the window and every arrival at it are
+  // known, and each destination can run all of the window's events on its own, in time
+  // order, with one set of cluster barriers per window instead of per event:
+  //   (1) event offsets of the window (own in-flight links; cluster OR of the bitmaps);
+  //   (2) the sorted offsets (at most kWinEv; a longer window is cut at the next event);
+  //   (3) all arrivals of the window applied to the held rows; each NPU's window arrivals
+  //       (offset, chunk) listed (pushed to the CTAs that mirror it); per-event delivery
+  //       counts summed over the cluster;
+  //   (4) done test: the first event whose cumulative deliveries reach `required` ends the
+  //       search there (no matching at it, as in the per-event loop);
+  //   (5) per destination, per event t_k < done: free / live in-links at t_k, Philox draws
+  //       (t_k, link, sigma), shorter-link-first ranks, the walk -- the source row at t_k is
+  //       the row after the window's arrivals minus the source's arrivals later than t_k;
+  //   (6) next window start = min busy_until of the links in flight (cluster MIN).
+  // V / D / M / E are counted per event exactly as in the per-event loop; the source-change
+  // versions count arrivals (hver[x] = arrivals at x before the window, plus its window
+  // arrivals up to t_k).  Send records go to the destination's own record range
+  // (Job::rec_off); emission sorts them by (t_start, link).
+  // ========================================================================================
+  bool windowed = false;
+  if constexpr (REG_PATH && P > 2 && !MASKED) {
+    if (lay.window != 0u) {
+      windowed = true;
+      uint32_t *w_bm = reinterpret_cast<uint32_t *>(smem + lay.off_wbm);
+      uint32_t *w_ev = reinterpret_cast<uint32_t *>(smem + lay.off_wev);
+      uint32_t *w_evc = reinterpret_cast<uint32_t *>(smem + lay.off_wevc);  // deliveries per event (cluster)
+      uint32_t *w_evo = reinterpret_cast<uint32_t *>(smem + lay.off_wevo);  // own deliveries per event
+      uint32_t *wa_cnt = reinterpret_cast<uint32_t *>(smem + lay.off_wacnt);
+      uint32_t *wa_off = reinterpret_cast<uint32_t *>(smem + lay.off_waoff);
+      uint16_t *wa_chk = reinterpret_cast<uint16_t *>(smem + lay.off_wachk);
+      uint32_t *rcnt = s_list;  // records written per own destination
+      const uint32_t Wwin = lay.window, DW = lay.win_deg, nbm = (Wwin + 31u) / 32u, kEv = lay.win_ev;
+      const uint32_t *rec_off = job.rec_off;
+      __shared__ uint32_t s_nev, s_wlim, s_kdone, s_wmin;
+      __shared__ unsigned long long s_wdel;
+      for (uint32_t i = tid; i < N; i += nthr) wa_cnt[i] = 0u;
+      for (uint32_t i = tid; i < nbm; i += nthr) w_bm[i] = 0u;
+      for (uint32_t i = tid; i < kWinEv; i += nthr) {
+        w_evc[i] = 0u;
+        w_evo[i] = 0u;
+      }
+      for (uint32_t i = d_lo + tid; i < d_hi; i += nthr) rcnt[i - d_lo] = 0u;
+      cluster_barrier();  // peers push into our bitmap / lists from now on
+      unsigned long long delivered = 0ull;  // cluster-wide deliveries before the window
+      for (;;) {
+        // ---- (1) event offsets of [t, t + W) ----
+        for (uint32_t q = p_lo + tid; q < p_hi; q += nthr)
+          if (cur[q] != kNone) {
+            const unsigned long long off = busy[q] - t;
+            if (off < Wwin) atomicOr(&w_bm[off >> 5], 1u << (off & 31u));
+          }
+        if (tid == 0) atomicOr(&w_bm[0], 1u);  // t itself
+        if (Q > 1) {
+          __syncthreads();
+          for (uint32_t i = tid; i < nbm; i += nthr) {
+            const uint32_t v = w_bm[i];
+            if (v)
+              for (uint32_t r = 0; r < Q; ++r)
+                if (r != crank) dsmem_or_b32(dsmem_addr(&w_bm[i], r), v);
+          }
+        }
+        cluster_barrier();
+        // ---- (2) sorted offsets, the window limit (first offset left out) ----
+        if (tid < 32) {
+          uint32_t n = 0;
+          if (lane == 0) s_wlim = Wwin;
+          for (uint32_t b = 0; b < nbm && n <= kEv; b += 32u) {
+            const uint32_t i = b + lane;
+            const uint32_t v = i < nbm ? w_bm[i] : 0u, c = __popc(v);
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+              if (lane >= (uint32_t)o) incl += y;
+            }
+            uint32_t pos = n + incl - c;
+            for (uint32_t m = v; m; m &= m - 1u, ++pos) {
+              const uint32_t off = i * 32u + (uint32_t)(__ffs(m) - 1);
+              if (pos < kEv) w_ev[pos] = off;
+              else if (pos == kEv) s_wlim = off;
+            }
+            n += __shfl_sync(0xFFFFFFFFu, incl, 31);
+          }
+          if (lane == 0) s_nev = n < kEv ? n : kEv;
+        }
+        __syncthreads();
+        const uint32_t n_ev = s_nev, wlim = s_wlim;
+        for (uint32_t i = tid; i < nbm; i += nthr) w_bm[i] = 0u;  // peers write it again after (6)
+        TCHECK(n_ev >= 1u && n_ev <= kEv && kEv <= kWinEv && w_ev[0] == 0u, "window events");
+        // ---- (3) arrivals of the window ----
+        {
+          uint32_t arr = 0;
+          for (uint32_t q = p_lo + tid; q < p_hi; q += nthr) {
+            const uint32_t c = cur[q];
+            if (c == kNone) continue;
+            const unsigned long long off64 = busy[q] - t;
+            if (off64 >= wlim) continue;
+            const uint32_t off = (uint32_t)off64, d = t_dst[q];
+            TCHECK(d < N && c < T.C, "window arrival");
+            atomicOr(&held[(size_t)d * Wr + (c >> 5)], 1u << (c & 31u));
+            const uint32_t j = atomicAdd(&wa_cnt[d], 1u);
+            TCHECK(j < DW, "window arrivals per NPU");
+            wa_off[d * DW + j] = off;
+            wa_chk[d * DW + j] = (uint16_t)c;
+            uint32_t lo = 0, hi = n_ev;  // event index of off (present in the list)
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (w_ev[mid] < off) lo = mid + 1u;
+              else hi = mid;
+            }
+            atomicAdd(&w_evo[lo], 1u);
+            cur[q] = kNone;
+            ++arr;
+            if (Q > 1)
+              for (uint32_t pm = s_peers[d]; pm; pm &= pm - 1u) {
+                const uint32_t r = __ffs(pm) - 1u;
+                if constexpr (ROWS_SMEM) dsmem_or_b32(dsmem_addr(&held[(size_t)d * Wr + (c >> 5)], r), 1u << (c & 31u));
+                dsmem_st_u32(dsmem_addr(&wa_off[d * DW + j], r), off);
+                dsmem_st_u16(dsmem_addr(&wa_chk[d * DW + j], r), (uint16_t)c);
+                dsmem_add_u32(dsmem_addr(&wa_cnt[d], r), 1u);
+              }
+          }
+          (void)arr;
+          __syncthreads();
+          for (uint32_t k = tid; k < n_ev; k += nthr) {  // per-event deliveries, summed over the cluster
+            const uint32_t v = w_evo[k];
+            if (v) {
+              atomicAdd(&w_evc[k], v);
+              for (uint32_t r = 0; r < Q; ++r)
+                if (r != crank) dsmem_add_u32(dsmem_addr(&w_evc[k], r), v);
+            }
+          }
+        }
+        cluster_barrier();
+        // ---- (4) done test inside the window ----
+        if (tid == 0) {
+          unsigned long long acc = delivered;
+          uint32_t kd = kNone;
+          for (uint32_t k = 0; k < n_ev; ++k) {
+            acc += w_evc[k];
+            if (acc == T.required) {
+              kd = k;
+              break;
+            }
+          }
+          s_kdone = kd;
+          unsigned long long tot = 0;
+          for (uint32_t k = 0; k < n_ev; ++k) tot += w_evc[k];
+          s_wdel = tot;
+          s_wmin = ~0u;
+        }
+        __syncthreads();
+        const uint32_t k_done = s_kdone;
+        const uint32_t n_run = k_done == kNone ? n_ev : k_done;
+        E += n_run;
+        // ---- (5) destinations: every event of the window before done ----
+        constexpr int SL = (kRegDeg + P - 1) / P;
+        for (uint32_t wi = tid / P; wi < d_hi - d_lo; wi += ngroups) {
+          const uint32_t d = d_lo + wi, b0 = s_inptr[d], b1 = s_inptr[d + 1], deg = b1 - b0;
+          TCHECK(b0 >= p_lo && b1 <= p_hi && deg <= kRegDeg, "window destination");
+          uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
+          uint4 hv[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+          unsigned long long bq[SL];
+          uint32_t sq[SL], srq[SL], hq[SL], nq[SL];
+#pragma unroll
+          for (int sl = 0; sl < SL; ++sl) {
+            const uint32_t j = (uint32_t)sl * P + gl, q = b0 + j;
+            const bool in = j < deg;
+            bq[sl] = in ? busy[q] : ~0ull;
+            sq[sl] = in ? seen[q] : 0u;
+            srq[sl] = in ? (uint32_t)t_src[q] : 0u;
+            hq[sl] = in ? hver[srq[sl]] : 0u;
+            nq[sl] = in ? wa_cnt[srq[sl]] : 0u;
+          }
+          uint32_t rc = rcnt[wi];
+          bool any_claim = false;
+          for (uint32_t k = 0; k < n_run; ++k) {
+            const uint32_t offk = w_ev[k];
+            const unsigned long long tk = t + offk;
+            unsigned long long key[SL];
+            uint32_t pk[SL], ver[SL];
+            uint32_t nfree = 0, nlive = 0;
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl) {
+              key[sl] = ~0ull;
+              pk[sl] = 0u;
+              ver[sl] = hq[sl];
+              const uint32_t j = (uint32_t)sl * P + gl;
+              if (j < deg && bq[sl] <= tk) {
+                ++nfree;
+                for (uint32_t a = 0; a < nq[sl]; ++a) ver[sl] += wa_off[srq[sl] * DW + a] <= offk ? 1u : 0u;
+                if (sq[sl] != ver[sl]) {
+                  const uint32_t q = b0 + j;
+                  const uint4 r = philox4x32_10(
+                      make_uint4((uint32_t)tk, (uint32_t)(tk >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
+                  key[sl] = ((unsigned long long)t_w[q] << 32) | r.x;  // (w, u_ord), R3
+                  pk[sl] = r.y;
+                  ++nlive;
+                }
+              }
+            }
+            nfree = __reduce_add_sync(gmask, nfree);
+            nlive = __reduce_add_sync(gmask, nlive);
+            if (gl == 0) {
+              myV += nfree;
+              myD += nfree ? 1u : 0u;
+            }
+            if (nlive == 0u) continue;
+            uint32_t rk[SL];
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl) rk[sl] = 0u;
+#pragma unroll
+            for (int i = 0; i < kRegDeg; ++i) {
+              const int isl = i / P, ilane = i % P;
+              const unsigned long long ki = __shfl_sync(gmask, key[isl], ilane, P);
+#pragma unroll
+              for (int sl = 0; sl < SL; ++sl) {
+                const uint32_t j = (uint32_t)sl * P + gl;
+                rk[sl] += (ki < key[sl] || (ki == key[sl] && (uint32_t)i < j)) ? 1u : 0u;
+              }
+            }
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl) rk[sl] = key[sl] != ~0ull ? rk[sl] : 0xFFu;
+            for (uint32_t s = 0; s < nlive; ++s) {
+              // the in-link of rank s: its slot, pick draw and source version (owner lane broadcasts)
+              uint32_t jj = 0, pp = 0, vv = 0;
+              bool own = false;
+#pragma unroll
+              for (int sl = 0; sl < SL; ++sl) {
+                const bool m = rk[sl] == s;
+                own = own || m;
+                jj = m ? (uint32_t)sl * P + gl : jj;
+                pp = m ? pk[sl] : pp;
+                vv = m ? ver[sl] : vv;
+              }
+              const int src_lane = __ffs(__ballot_sync(gmask, own)) - 1;
+              jj = __shfl_sync(gmask, jj, src_lane);
+              pp = __shfl_sync(gmask, pp, src_lane);
+              vv = __shfl_sync(gmask, vv, src_lane);
+              const uint32_t q = b0 + jj, sp = t_src[q];
+              uint4 cv[V];
+              const uint4 *h4 = reinterpret_cast<const uint4 *>(held + (size_t)sp * Wr);
+#pragma unroll
+              for (int v = 0; v < V; ++v) cv[v] = ROWS_SMEM ? h4[v * P + gl] : __ldcg(&h4[v * P + gl]);
+              // the source's arrivals after t_k are not held yet at t_k
+              const uint32_t na = wa_cnt[sp];
+              for (uint32_t a = 0; a < na; ++a) {
+                if (wa_off[sp * DW + a] <= offk) continue;
+                const uint32_t c = wa_chk[sp * DW + a], wd = c >> 5, vec = wd >> 2;
+                if (vec % P != gl) continue;
+                const uint32_t vi = vec / P, comp = wd & 3u, nb = ~(1u << (c & 31u));
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                  if ((uint32_t)v != vi) continue;
+                  cv[v].x &= comp == 0u ? nb : ~0u;
+                  cv[v].y &= comp == 1u ? nb : ~0u;
+                  cv[v].z &= comp == 2u ? nb : ~0u;
+                  cv[v].w &= comp == 3u ? nb : ~0u;
+                }
+              }
+              uint32_t incl[V], tot[V], K = 0;
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                cv[v] = andnot4(cv[v], hv[v]);  // held[src](t_k) & ~have[d]
+                incl[v] = popc4(cv[v]);
+#pragma unroll
+                for (int o = 1; o < P; o <<= 1) {
+                  const uint32_t y = __shfl_up_sync(gmask, incl[v], o, P);
+                  if (gl >= (uint32_t)o) incl[v] += y;
+                }
+                tot[v] = __shfl_sync(gmask, incl[v], P - 1, P);
+                K += tot[v];
+              }
+              const uint32_t osl = jj / P;  // slot of the in-link on its owner lane
+              if (K == 0u) {  // exact skip from here on while the source is unchanged
+                if (gl == jj % P) {
+#pragma unroll
+                  for (int sl = 0; sl < SL; ++sl)
+                    if ((uint32_t)sl == osl) sq[sl] = vv;
+                  seen[q] = vv;
+                }
+                continue;
+              }
+              uint32_t rv = __umulhi(pp, K);  // floor(u_pick * K / 2^32), R13
+              int vsel = 0;
+#pragma unroll
+              for (int v = 0; v + 1 < V; ++v) {
+                const bool adv = (vsel == v) && (rv >= tot[v]);
+                rv = adv ? rv - tot[v] : rv;
+                vsel = adv ? v + 1 : vsel;
+              }
+              uint4 x = cv[0];
+              uint32_t inc = incl[0];
+#pragma unroll
+              for (int v = 1; v < V; ++v) {
+                x = (vsel == v) ? cv[v] : x;
+                inc = (vsel == v) ? incl[v] : inc;
+              }
+              const uint32_t cx = __popc(x.x), cy = __popc(x.y), cz = __popc(x.z);
+              const uint32_t excl = inc - (cx + cy + cz + __popc(x.w));
+              const bool mine = (rv >= excl) && (rv < inc);
+              uint32_t rr = rv - excl, wsel = 0, word = x.x;
+              bool m = rr >= cx;
+              rr = m ? rr - cx : rr; wsel = m ? 1u : wsel; word = m ? x.y : word;
+              m = m && rr >= cy;
+              rr = m ? rr - cy : rr; wsel = m ? 2u : wsel; word = m ? x.z : word;
+              m = m && rr >= cz;
+              rr = m ? rr - cz : rr; wsel = m ? 3u : wsel; word = m ? x.w : word;
+              const uint32_t bit = select_bit_swar(word, rr);
+              const uint32_t mask = mine ? (1u << bit) : 0u;
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                if (vsel != v) continue;
+                hv[v].x |= wsel == 0u ? mask : 0u;
+                hv[v].y |= wsel == 1u ? mask : 0u;
+                hv[v].z |= wsel == 2u ? mask : 0u;
+                hv[v].w |= wsel == 3u ? mask : 0u;
+              }
+              uint32_t chunk = (((uint32_t)vsel * P + gl) * 4u + wsel) * 32u + bit;
+              chunk = __shfl_sync(gmask, chunk, __ffs(__ballot_sync(gmask, mine)) - 1);
+              TCHECK(chunk < T.C, "window claim");
+              const uint32_t wp = t_w[q];
+              if (gl == jj % P) {  // the slot's owner lane: link state
+#pragma unroll
+                for (int sl = 0; sl < SL; ++sl)
+                  if ((uint32_t)sl == osl) bq[sl] = tk + wp;
+                cur[q] = chunk;
+                busy[q] = tk + wp;
+              }
+              if (gl == 0) {
+                ++myM;
+                if (rec != nullptr) {
+                  TCHECK(rec_off[d] + rc < rec_off[d + 1], "window record");
+                  Rec r;
+                  r.chunk = chunk;
+                  r.link = t_lid[q];
+                  r.t_start = tk;
+                  rec[rec_off[d] + rc] = r;
+                }
+              }
+              ++rc;
+              any_claim = true;
+            }
+          }
+          if (any_claim) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) have4[v * P + gl] = hv[v];
+            if (gl == 0) rcnt[wi] = rc;
+          }
+        }
+        __syncthreads();
+        // ---- (6) end of the window ----
+        delivered += s_wdel;
+        for (uint32_t x = tid; x < N; x += nthr) {
+          const uint32_t a = wa_cnt[x];
+          if (a) {
+            hver[x] += a;
+            wa_cnt[x] = 0u;
+          }
+        }
+        for (uint32_t k = tid; k < n_ev; k += nthr) {
+          w_evc[k] = 0u;
+          w_evo[k] = 0u;
+        }
+        if (k_done != kNone) {
+          t += w_ev[k_done];
+          break;
+        }
+        // next window start: min busy_until over the links in flight (offsets < 2^32: w < 2^31)
+        uint32_t mo = ~0u;
+        for (uint32_t q = p_lo + tid; q < p_hi; q += nthr)
+          if (cur[q] != kNone) {
+            const uint32_t o = (uint32_t)(busy[q] - t);
+            mo = o < mo ? o : mo;
+          }
+        mo = __reduce_min_sync(0xFFFFFFFFu, mo);
+        if (lane == 0 && mo != ~0u) atomicMin(&s_wmin, mo);
+        __syncthreads();
+        if (Q > 1 && tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid), (unsigned long long)s_wmin << 32);
+        cluster_barrier();
+        uint32_t mo_all = s_wmin;
+        if (Q > 1) {
+          mo_all = ~0u;
+          for (uint32_t r = 0; r < Q; ++r) {
+            const uint32_t hi = (uint32_t)(s_slot_min[r] >> 32);
+            mo_all = hi < mo_all ? hi : mo_all;
+          }
+        }
+        if (mo_all == ~0u) {  // nothing in flight and not done: stall (R17)
+          status = -3;
+          break;
+        }
+        t += mo_all;
+        if (t >= kMaxTime) {
+          status = -6;
+          break;
+        }
+        ++e;
+      }
+    }
+  }
+
+  if (!windowed)
   for (;;) {
     long long ts[9];  // debug phase timestamps (TACOS_TRACE), thread 0
     if (tracing) ts[0] = clock64();
@@ -1075,6 +1484,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             lv[q] = f;
           }
           nfree += f ? 1u : 0u;
+          if (P == 1 && f == 2) order[b0 + nl] = (uint16_t)(q - b0);  // one lane: compact list of the live in-links
           nl += f == 2 ? 1u : 0u;
         }
         if (P > 1) {
@@ -1086,6 +1496,34 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           myD += nfree ? 1u : 0u;
         }
         if (nl == 0u) continue;
+        if constexpr (P == 1) {
+          // one lane per destination: the walk takes the live in-links in shorter-link-first order
+          // (R3: smallest (w, u_ord, position) first, positions ascend with the link id) by a
+          // selection over the compact live list -- O(live^2) instead of O(live x in-degree)
+#pragma unroll
+          for (int v = 0; v < V; ++v) if (!kHaveSmem) hv[v] = have4[v];
+          for (uint32_t s = 0; s < nl; ++s) {
+            uint32_t bi = s, bp = b0 + order[b0 + s];
+            unsigned long long bk = ((unsigned long long)t_w[bp] << 32) | ord[bp];
+            for (uint32_t i = s + 1; i < nl; ++i) {
+              const uint32_t qi = b0 + order[b0 + i];
+              const unsigned long long ki = ((unsigned long long)t_w[qi] << 32) | ord[qi];
+              const bool better = ki < bk || (ki == bk && qi < bp);
+              bi = better ? i : bi;
+              bp = better ? qi : bp;
+              bk = better ? ki : bk;
+            }
+            if (bi != s) {
+              const uint16_t tmp = order[b0 + s];
+              order[b0 + s] = order[b0 + bi];
+              order[b0 + bi] = tmp;
+            }
+            step(bp, pick[bp]);
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v] = hv[v];
+          continue;
+        }
         if (P > 1) __syncwarp(gmask);
         // shorter-link-first order of the live in-links (R3): rank by (w, u_ord, link)
         for (uint32_t q = b0 + gl; q < b1; q += P) {

@@ -470,6 +470,7 @@ struct Part {
   uint32_t N = 0, L = 0, C = 0, k = 0, Wp = 0, P = 0, VPL = 0;
   bool custom = false, symmetric = false, rs_search = false;
   uint32_t rs_base = 0;  // first job of the G^T (sigma 1) search: S, or 0 when only the RS phase is searched
+  bool windowed = false;  // searched by the windowed event loop (records per destination, sorted at emission)
   uint64_t required = 0;
   uint64_t cap = 0;  // send records per job (= required without relays)
   std::vector<uint32_t> w;
@@ -478,6 +479,7 @@ struct Part {
   uint32_t *d_w = nullptr;
   uint32_t job_base = 0, n_jobs = 0;  // jobs [job_base, job_base + n_jobs): S (sigma 0) then S (sigma 1)
   Rec *d_rec = nullptr;               // n_jobs * required records
+  const uint32_t *d_rec_off = nullptr;  // windowed loop: per-destination record offsets (N + 1)
   uint64_t *d_keys = nullptr;         // 2
   uint64_t *d_stats = nullptr;        // 5
   uint64_t *d_times_ag = nullptr, *d_times_rs = nullptr;
@@ -681,10 +683,10 @@ uint32_t pow2_at_least(uint32_t x) {
 // occupancy queries.
 struct ClusterKey {
   int dev;
-  uint32_t N, L, W, P, V, jobs, reg_path, masked, worklist, smem;
+  uint32_t N, L, W, P, V, jobs, reg_path, masked, worklist, smem, win, deg;
   bool operator<(const ClusterKey &o) const {
-    return std::tie(dev, N, L, W, P, V, jobs, reg_path, masked, worklist, smem) <
-           std::tie(o.dev, o.N, o.L, o.W, o.P, o.V, o.jobs, o.reg_path, o.masked, o.worklist, o.smem);
+    return std::tie(dev, N, L, W, P, V, jobs, reg_path, masked, worklist, smem, win, deg) <
+           std::tie(o.dev, o.N, o.L, o.W, o.P, o.V, o.jobs, o.reg_path, o.masked, o.worklist, o.smem, o.win, o.deg);
   }
 };
 std::mutex g_cluster_mu;
@@ -868,6 +870,38 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     }
     g.lay.worklist = (multi_w && g.lay.reg_path) ? 1u : 0u;  // measured: helps the mesh (config 4), not config 5
     if (const char *env = getenv("TACOS_WORKLIST")) g.lay.worklist = (uint32_t)atoi(env);
+    // Windowed event loop (greedy_kernel.cuh): several link costs, wide rows on the
+    // register path, no relays, link-first; window W = the group's smallest link cost (capped),
+    // every cost < 2^31 (busy offsets from a window start stay below 2^32).  TACOS_WINDOW=0: off.
+    uint32_t win = 0;
+    {
+      uint32_t w_min = ~0u, w_max = 0;
+      for (size_t gk = gi; gk < gj; ++gk)
+        for (uint32_t x : pl->parts[order[gk]].w) {
+          w_min = std::min(w_min, x);
+          w_max = std::max(w_max, x);
+        }
+      const char *env = getenv("TACOS_WINDOW");
+      const bool want = env ? atoi(env) != 0 : true;
+      if (want && multi_w && g.lay.reg_path && P0 > 2 && !relay && !(p->flags & TACOS_FLAG_LITERAL) &&
+          w_max < (1u << 31))
+        win = std::min<uint32_t>(w_min, kWinBits);
+    }
+    auto finish_layout = [&](Layout &lq) {
+      lq.reg_path = g.lay.reg_path;
+      lq.masked = g.lay.masked;
+      lq.worklist = g.lay.worklist;
+      add_window(lq, maxN, win, max_deg);
+      if (win && (size_t)lq.smem_bytes > smem_limit) {  // does not fit: the per-event loop
+        Layout l2 = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, n_jobs - begin, (uint32_t)n_sms, lq.cluster);
+        l2.reg_path = lq.reg_path;
+        l2.masked = lq.masked;
+        l2.worklist = lq.worklist;
+        add_window(l2, maxN, 0, 0);
+        lq = l2;
+      }
+    };
+    finish_layout(g.lay);
     // Cluster size: the largest Q <= 8 (any size, not only powers of two) with jobs * Q <= #SMs,
     // >= 64 destinations per CTA, and every job's cluster co-resident on the chip (asked of the
     // occupancy calculator for the kernel this layout selects: only 15 clusters of 8 fit on a
@@ -875,14 +909,12 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     // would double the time). TACOS_CLUSTER overrides.
     // (the choice is cached per shape: the occupancy queries cost more than a small synthesis)
     const ClusterKey ck{dev, maxN, maxL, maxW, P0, V0, n_jobs - begin, g.lay.reg_path, g.lay.masked, g.lay.worklist,
-                        (uint32_t)smem_limit};
+                        (uint32_t)smem_limit, win, max_deg};
     uint32_t cached_q = 0;
     if (!(p->flags & TACOS_FLAG_LITERAL) && !getenv("TACOS_CLUSTER") && cluster_cache_get(ck, &cached_q)) {
       if (cached_q != g.lay.cluster) {
         Layout lq = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, n_jobs - begin, (uint32_t)n_sms, cached_q);
-        lq.reg_path = g.lay.reg_path;
-        lq.masked = g.lay.masked;
-        lq.worklist = g.lay.worklist;
+        finish_layout(lq);
         g.lay = lq;
       }
     } else if (!(p->flags & TACOS_FLAG_LITERAL) && !getenv("TACOS_CLUSTER")) {
@@ -890,9 +922,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       for (uint32_t q = 8; q > g.lay.cluster; --q) {
         if ((uint64_t)jobs * q > (uint64_t)n_sms || maxN / q < 64u) continue;
         Layout lq = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, jobs, (uint32_t)n_sms, q);
-        lq.reg_path = g.lay.reg_path;
-        lq.masked = g.lay.masked;
-        lq.worklist = g.lay.worklist;
+        finish_layout(lq);
         int n_active = 0;
         g_occ_query = &n_active;
         launch_greedy(lq, P0, V0, nullptr, jobs, nullptr, nullptr);
@@ -909,6 +939,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
                   smem_limit);
     g.job_begin = begin;
     g.job_end = n_jobs;
+    for (size_t gk = gi; gk < gj; ++gk) pl->parts[order[gk]].windowed = g.lay.window != 0u;
     pl->groups.push_back(g);
     gi = gj;
   }
@@ -937,7 +968,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.cap * pt.n_jobs, &vp))) return rc;
       pt.d_rec = reinterpret_cast<Rec *>(vp);
     }
-    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL)) && record) max_M = std::max(max_M, pt.cap);
+    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL) || pt.windowed) && record) max_M = std::max(max_M, pt.cap);
   }
   if (max_M) {
     pl->sort_bytes = rs_sort_scratch_bytes(max_M);
@@ -946,7 +977,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   PlanStage sg;
   const size_t o_outs = sg.reserve(sizeof(JobOut) * n_jobs), o_count = sg.reserve(8);
   struct PartOffs {
-    size_t w, pos_w[2], allow[2] = {0, 0}, pre = 0, post = 0, topo[2], keys, times_ag, times_rs = 0;
+    size_t w, pos_w[2], allow[2] = {0, 0}, pre = 0, post = 0, topo[2], keys, times_ag, times_rs = 0, rec_off = 0;
   };
   std::vector<PartOffs> po(n_topos);
   for (uint32_t i = 0; i < n_topos; ++i) {
@@ -976,6 +1007,22 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         }
       o.pre = sg.add(pre_p.data(), pre_p.size() * 4);
       o.post = sg.add(post_p.data(), post_p.size() * 4);
+    }
+    if (pt.windowed) {  // records of destination x at [rec_off[x], rec_off[x+1]): |post[x] - pre[x]| each
+      std::vector<uint32_t> ro(pt.N + 1, 0u);
+      const uint32_t W0 = (pt.C + 31u) / 32u;
+      for (uint32_t x = 0; x < pt.N; ++x) {
+        uint32_t need;
+        if (custom) {
+          need = 0;
+          for (uint32_t q = 0; q < W0; ++q)
+            need += (uint32_t)__builtin_popcount(pl->post[(size_t)x * W0 + q] & ~pl->pre[(size_t)x * W0 + q]);
+        } else {
+          need = pt.C - pt.k;
+        }
+        ro[x + 1] = ro[x] + need;
+      }
+      o.rec_off = sg.add(ro.data(), ro.size() * 4);
     }
     for (int q = 0; q < 2; ++q) o.topo[q] = sg.reserve(sizeof(DevTopo));
     o.keys = sg.reserve(8 * 8);
@@ -1013,6 +1060,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       sg.put(o.topo[q], h);
       pt.d_topo[q] = reinterpret_cast<DevTopo *>(base + o.topo[q]);
     }
+    pt.d_rec_off = pt.windowed ? reinterpret_cast<const uint32_t *>(base + o.rec_off) : nullptr;
     pt.d_keys = reinterpret_cast<uint64_t *>(base + o.keys);
     pt.d_stats = pt.d_keys + 2;
     pt.d_times_ag = reinterpret_cast<uint64_t *>(base + o.times_ag);
@@ -1035,6 +1083,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         jb.out_slot = pt.job_base + j;
         jb.rec = record ? pt.d_rec + (size_t)j * pt.cap : nullptr;
         jb.rec_cap = record ? pt.cap : 0;
+        jb.rec_off = pt.d_rec_off;
         jb.g_rows = nullptr;
         jb.g_links = nullptr;
         jb.trace = nullptr;
@@ -1189,7 +1238,7 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
     uint32_t nl = 0;
     // one link cost, symmetric, no relays: the mirror order needs no sort (launch_rs_uniform_emit)
     // (its link-id bitmap lives in shared memory: 2 bits per link, at most 200 KB)
-    const bool uniform = pt.symmetric && !coll_relay(&pl->p) && !pt.w.empty() &&
+    const bool uniform = pt.symmetric && !coll_relay(&pl->p) && !pt.windowed && !pt.w.empty() &&
                          (size_t)8 * ((pt.L + 31u) / 32u) <= (size_t)200 * 1024 &&
                          std::all_of(pt.w.begin(), pt.w.end(), [&](uint32_t x) { return x == pt.w[0]; });
     if (uniform) {
@@ -1208,7 +1257,7 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
     if ((rc = job_matches((uint32_t)(g_ag - off), &M))) return rc;
     const Rec *rec = pt.d_rec + (size_t)(g_ag - off) * pt.cap;
     const uint64_t base = coll == TACOS_ALL_REDUCE ? pt.required : 0;  // AR: after the RS half (no relays)
-    if (pl->p.flags & TACOS_FLAG_LITERAL) {  // records in delivery order: sort by (t_start, link)
+    if ((pl->p.flags & TACOS_FLAG_LITERAL) || pt.windowed) {  // records not in (t_start, link) order: sort
       uint32_t nl = 0;
       if ((rc = launch_rs_sort_emit(rec, M, pt.td->d_src, pt.td->d_dst, pt.d_w, nullptr, T_ag, pt.L, d_sends + base, pl->d_sort,
                                     pl->sort_bytes, &nl, st, /*mirror=*/0u, /*shift=*/T_rs)))

@@ -46,6 +46,7 @@ struct Job {
   uint64_t seed;
   uint32_t sigma;
   uint32_t out_slot;
+  const uint32_t *rec_off;  // windowed loop: records of destination d at [rec_off[d], rec_off[d+1])
   Rec *rec;              // nullptr: recording off
   uint64_t rec_cap;      // records the job may write (bounds-checked build)
   uint32_t *g_rows;      // global rows (held | have) when they do not fit in smem
@@ -81,7 +82,15 @@ struct Layout {
   uint32_t reg_path;     // 1: every in-degree <= 8 (register ranking path)
   uint32_t worklist;     // 1: compact the destinations with a live in-link before matching
   uint32_t masked;       // 1: relays (R22): candidates & allow[p], only required arrivals count
+  // windowed event loop (greedy_window.cuh): window length W in time units (0 = one event per
+  // iteration), max in-degree, and its shared-memory arrays (after the others)
+  uint32_t window, win_deg, win_ev;  // win_ev: events per window at most (<= kWinEv; TACOS_WIN_EV)
+  uint32_t off_wbm, off_wev, off_wevc, off_wevo, off_wacnt, off_waoff, off_wachk;
 };
+constexpr uint32_t kWinEv = 256;      // events per window at most (a longer window is cut there)
+constexpr uint32_t kWinBits = 16384;  // window length cap (bitmap of event offsets)
+// Append the windowed loop's shared-memory arrays to a layout (window = W, deg = max in-degree).
+void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg);
 
 // q_force: cluster size to use (0: the automatic choice; TACOS_CLUSTER overrides both)
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,

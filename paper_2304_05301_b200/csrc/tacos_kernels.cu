@@ -121,6 +121,27 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   return lay;
 }
 
+void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg) {
+  auto al = [](uint32_t x, uint32_t a) { return (x + a - 1u) / a * a; };
+  lay.window = window;
+  lay.win_deg = deg;
+  lay.win_ev = kWinEv;
+  if (const char *env = getenv("TACOS_WIN_EV")) {  // testing: shorter windows (cut at the n-th event)
+    const int n = atoi(env);
+    if (n >= 1 && n <= (int)kWinEv) lay.win_ev = (uint32_t)n;
+  }
+  if (!window) return;
+  uint32_t s = lay.smem_bytes;
+  lay.off_wbm = s; s += al((window + 31u) / 32u * 4u, 16u);
+  lay.off_wev = s; s += kWinEv * 4u;
+  lay.off_wevc = s; s += kWinEv * 4u;
+  lay.off_wevo = s; s += kWinEv * 4u;
+  lay.off_wacnt = s; s += al(N * 4u, 16u);
+  lay.off_waoff = s; s += al(N * deg * 4u, 16u);
+  lay.off_wachk = s; s += al(N * deg * 2u, 16u);
+  lay.smem_bytes = s;
+}
+
 int launch_greedy(const Layout &lay, uint32_t P, uint32_t VPL, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs,
                   void *stream) {
   cudaStream_t st = (cudaStream_t)stream;

@@ -383,3 +383,50 @@ def test_forced_cluster_splits(T, monkeypatch, q, case):
     monkeypatch.setenv("TACOS_CLUSTER", str(q))
     syn, sch, _ = run_both(T, topo, k, 1 << 20, coll, seeds)
     assert_parity(syn, sch, coll)
+
+
+# --------------------------------------------------------------------------
+# the windowed event loop (several link costs, wide rows): bit-exact with the oracle,
+# with windows cut short (TACOS_WIN_EV), with every cluster size, against the per-event loop
+# --------------------------------------------------------------------------
+def _window_case(name):
+    if name == "mesh16x16_k8":
+        return W.mesh2d(16, 16, 200, 100), 8, "AR", 4
+    if name == "rand16_distinct_costs_k128":  # asymmetric, ~40 distinct costs: many events per window
+        topo = W.random_strongly_connected(16, 40, 11, bws=(25, 50, 100, 200), alphas=tuple(range(0, 20000, 37)))
+        return topo, 128, "AR", 3
+    if name == "mesh8x8_k32_rs":
+        return W.mesh2d(8, 8, 200, 100), 32, "RS", 3
+    raise ValueError(name)
+
+
+@pytest.mark.parametrize("win_ev", ["256", "2"])
+@pytest.mark.parametrize("name", ["mesh16x16_k8", "rand16_distinct_costs_k128", "mesh8x8_k32_rs"])
+def test_windowed_loop_parity(T, monkeypatch, name, win_ev):
+    topo, k, coll, seeds = _window_case(name)
+    indeg = np.bincount(topo.dst, minlength=topo.n_npus)
+    assert indeg.max() <= 8  # register path (the windowed loop's domain)
+    monkeypatch.setenv("TACOS_WIN_EV", win_ev)
+    syn, sch, t = run_both(T, topo, k, 128 << 10, coll, seeds)
+    assert_parity(syn, sch, coll)
+    p, keep = T.make_params(coll, k, 128 << 10, seeds)
+    plan = T.Plan(t, coll, k, 128 << 10, seeds)
+    assert plan.info()["n_jobs"] >= seeds
+
+
+@pytest.mark.parametrize("q", [1, 3, 8])
+def test_windowed_loop_cluster_sizes(T, monkeypatch, q):
+    monkeypatch.setenv("TACOS_CLUSTER", str(q))
+    syn, sch, _ = run_both(T, W.mesh2d(16, 16, 200, 100), 8, 128 << 10, "AR", 3)
+    assert_parity(syn, sch, "AR")
+
+
+def test_windowed_loop_equals_per_event_loop(T, monkeypatch):
+    """Same schedules, times and counters with the window off (TACOS_WINDOW=0)."""
+    topo, k, coll, seeds = _window_case("rand16_distinct_costs_k128")
+    t = T.Topology.from_workload_topology(topo)
+    a = T.synthesize(t, coll, k, 128 << 10, seeds, keep_seed_times=True)
+    monkeypatch.setenv("TACOS_WINDOW", "0")
+    b = T.synthesize(t, coll, k, 128 << 10, seeds, keep_seed_times=True)
+    assert a.sends.tobytes() == b.sends.tobytes() and a.result == b.result
+    assert np.array_equal(a.seed_times, b.seed_times)
