@@ -495,7 +495,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
           uint32_t rc = rcnt[wi];
           bool any_claim = false;
-          for (uint32_t k = 0; k < n_run; ++k) {
+          // Only the events at which this destination's state can change are run: an arrival
+          // at d (an in-link frees) or at the source of an in-link (the source's row grows).  In
+          // between, no in-link is live (each was matched, is busy or has an unchanged source
+          // since its last empty visit), so those events only add the free-link count to V / D.
+          uint32_t k = 0;
+          while (k < n_run) {
             const uint32_t offk = w_ev[k];
             const unsigned long long tk = t + offk;
             unsigned long long key[SL];
@@ -520,13 +525,17 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                 }
               }
             }
-            nfree = __reduce_add_sync(gmask, nfree);
-            nlive = __reduce_add_sync(gmask, nlive);
+            {  // one group reduction for both counts (each <= kRegDeg)
+              const uint32_t both = __reduce_add_sync(gmask, (nfree << 16) | nlive);
+              nfree = both >> 16;
+              nlive = both & 0xFFFFu;
+            }
             if (gl == 0) {
               myV += nfree;
               myD += nfree ? 1u : 0u;
             }
-            if (nlive == 0u) continue;
+            const uint32_t rc_event = rc;
+            if (nlive != 0u) {
             uint32_t rk[SL];
 #pragma unroll
             for (int sl = 0; sl < SL; ++sl) rk[sl] = 0u;
@@ -662,6 +671,36 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               ++rc;
               any_claim = true;
             }
+            }  // nlive
+            // the next event that can change this destination's state, and the free in-links
+            // until then (this event's claims are busy now)
+            const uint32_t nf = nfree - (rc - rc_event);  // every claim of this event took a free in-link
+            uint32_t nx = ~0u;
+#pragma unroll
+            for (int sl = 0; sl < SL; ++sl) {
+              const uint32_t j = (uint32_t)sl * P + gl;
+              if (j >= deg) continue;
+              if (bq[sl] > tk) {
+                const unsigned long long o = bq[sl] - t;
+                if (o < wlim && (uint32_t)o < nx) nx = (uint32_t)o;
+              }
+              for (uint32_t a = 0; a < nq[sl]; ++a) {
+                const uint32_t o = wa_off[srq[sl] * DW + a];
+                if (o > offk && o < nx) nx = o;
+              }
+            }
+            nx = __reduce_min_sync(gmask, nx);
+            uint32_t lo = k + 1u, hi = n_run;  // first event at or after offset nx
+            while (lo < hi) {
+              const uint32_t mid = (lo + hi) >> 1;
+              if (w_ev[mid] < nx) lo = mid + 1u;
+              else hi = mid;
+            }
+            if (gl == 0) {
+              myV += (unsigned long long)nf * (lo - k - 1u);
+              myD += nf ? (unsigned long long)(lo - k - 1u) : 0ull;
+            }
+            k = lo;
           }
           if (any_claim) {
 #pragma unroll
