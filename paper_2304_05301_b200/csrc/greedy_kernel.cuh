@@ -350,7 +350,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       uint32_t *rcnt = s_list;  // records written per own destination
       const uint32_t Wwin = lay.window, DW = lay.win_deg, nbm = (Wwin + 31u) / 32u, kEv = lay.win_ev;
       const uint32_t *rec_off = job.rec_off;
-      __shared__ uint32_t s_nev, s_wlim, s_kdone, s_wmin;
+      __shared__ uint32_t s_nev, s_wlim, s_kdone, s_wmin, s_wnext;
       __shared__ unsigned long long s_wdel;
       for (uint32_t i = tid; i < N; i += nthr) wa_cnt[i] = 0u;
       for (uint32_t i = tid; i < nbm; i += nthr) w_bm[i] = 0u;
@@ -467,6 +467,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (uint32_t k = 0; k < n_ev; ++k) tot += w_evc[k];
           s_wdel = tot;
           s_wmin = ~0u;
+          s_wnext = 0u;
         }
         __syncthreads();
         const uint32_t k_done = s_kdone;
@@ -474,7 +475,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         E += n_run;
         // ---- (5) destinations: every event of the window before done ----
         constexpr int SL = (kRegDeg + P - 1) / P;
-        for (uint32_t wi = tid / P; wi < d_hi - d_lo; wi += ngroups) {
+        // destinations are taken from a shared counter, one group at a time: their costs differ
+        // widely inside a window, and a static split left groups waiting at the barrier
+        for (;;) {
+          uint32_t wi = 0;
+          if (gl == 0) wi = atomicAdd(&s_wnext, 1u);
+          wi = __shfl_sync(gmask, wi, 0, P);
+          if (wi >= d_hi - d_lo) break;
           const uint32_t d = d_lo + wi, b0 = s_inptr[d], b1 = s_inptr[d + 1], deg = b1 - b0;
           TCHECK(b0 >= p_lo && b1 <= p_hi && deg <= kRegDeg, "window destination");
           uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
@@ -483,6 +490,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
           unsigned long long bq[SL];
           uint32_t sq[SL], srq[SL], hq[SL], nq[SL];
+          // the first kWinReg window-arrival offsets of each slot's source, in registers (~0 = none)
+          constexpr int kWinReg = 4;
+          uint32_t ao[SL][kWinReg];
 #pragma unroll
           for (int sl = 0; sl < SL; ++sl) {
             const uint32_t j = (uint32_t)sl * P + gl, q = b0 + j;
@@ -492,6 +502,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             srq[sl] = in ? (uint32_t)t_src[q] : 0u;
             hq[sl] = in ? hver[srq[sl]] : 0u;
             nq[sl] = in ? wa_cnt[srq[sl]] : 0u;
+#pragma unroll
+            for (int a = 0; a < kWinReg; ++a) ao[sl][a] = (uint32_t)a < nq[sl] ? wa_off[srq[sl] * DW + a] : ~0u;
           }
           uint32_t rc = rcnt[wi];
           bool any_claim = false;
@@ -514,7 +526,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               const uint32_t j = (uint32_t)sl * P + gl;
               if (j < deg && bq[sl] <= tk) {
                 ++nfree;
-                for (uint32_t a = 0; a < nq[sl]; ++a) ver[sl] += wa_off[srq[sl] * DW + a] <= offk ? 1u : 0u;
+#pragma unroll
+                for (int a = 0; a < kWinReg; ++a) ver[sl] += ao[sl][a] <= offk ? 1u : 0u;
+                for (uint32_t a = kWinReg; a < nq[sl]; ++a) ver[sl] += wa_off[srq[sl] * DW + a] <= offk ? 1u : 0u;
                 if (sq[sl] != ver[sl]) {
                   const uint32_t q = b0 + j;
                   const uint4 r = philox4x32_10(
@@ -684,7 +698,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                 const unsigned long long o = bq[sl] - t;
                 if (o < wlim && (uint32_t)o < nx) nx = (uint32_t)o;
               }
-              for (uint32_t a = 0; a < nq[sl]; ++a) {
+#pragma unroll
+              for (int a = 0; a < kWinReg; ++a) {
+                const uint32_t o = ao[sl][a];
+                if (o > offk && o < nx) nx = o;
+              }
+              for (uint32_t a = kWinReg; a < nq[sl]; ++a) {
                 const uint32_t o = wa_off[srq[sl] * DW + a];
                 if (o > offk && o < nx) nx = o;
               }
