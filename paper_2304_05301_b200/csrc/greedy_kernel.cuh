@@ -486,8 +486,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           TCHECK(b0 >= p_lo && b1 <= p_hi && deg <= kRegDeg, "window destination");
           uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
           uint4 hv[V];
-#pragma unroll
-          for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+          bool hv_loaded = false;  // the have row (L2 with global rows) is read at the first live event
           unsigned long long bq[SL];
           uint32_t sq[SL], srq[SL], hq[SL], nq[SL];
           // the first kWinReg window-arrival offsets of each slot's source, in registers (~0 = none)
@@ -549,6 +548,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               myD += nfree ? 1u : 0u;
             }
             const uint32_t rc_event = rc;
+            if (nlive != 0u && !hv_loaded) {
+#pragma unroll
+              for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+              hv_loaded = true;
+            }
             if (nlive != 0u) {
             uint32_t rk[SL];
 #pragma unroll
