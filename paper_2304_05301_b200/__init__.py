@@ -75,7 +75,8 @@ class tacos_result(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("rs_seed", ctypes.c_uint64), ("n_sends", ctypes.c_uint64),
                 ("matches", ctypes.c_uint64), ("visits", ctypes.c_uint64), ("dest_events", ctypes.c_uint64),
                 ("events", ctypes.c_uint64), ("status", ctypes.c_int32), ("winner_local", ctypes.c_uint32),
-                ("best_key_ag", ctypes.c_uint64), ("best_key_rs", ctypes.c_uint64), ("cancelled", ctypes.c_uint64)]
+                ("best_key_ag", ctypes.c_uint64), ("best_key_rs", ctypes.c_uint64), ("cancelled", ctypes.c_uint64),
+                ("live_visits", ctypes.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -84,10 +84,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   extern __shared__ __align__(16) unsigned char smem[];
   // 64-bit shared atomics are CAS loops on sm_100a: per-event values use 32-bit atomics
   // (arrivals of one event; next event time as an offset from t, < 2^32 since w < 2^32)
-  __shared__ unsigned long long s_delivered, s_V, s_D, s_M;
+  __shared__ unsigned long long s_delivered, s_V, s_D, s_M, s_L;
   __shared__ uint32_t s_arr[2], s_min32[2], s_mcnt[2];
   // cluster exchange slots, indexed by the writer's rank (plain remote stores, no 64-bit DSMEM atomics)
-  __shared__ unsigned long long s_slot_deliv[8], s_slot_min[8], s_slot_cnt[8][3];
+  __shared__ unsigned long long s_slot_deliv[8], s_slot_min[8], s_slot_cnt[8][4];
 
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -215,7 +215,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   if (tid == 0) {
     s_delivered = 0ull;
     s_arr[0] = s_arr[1] = 0u;
-    s_V = s_D = s_M = 0ull;
+    s_V = s_D = s_M = s_L = 0ull;
   }
   cluster_barrier();  // peers may add to our counters / mirror lists from now on
   if (Q > 1) {  // register as a mirror of the remote sources of own in-links
@@ -229,7 +229,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   unsigned long long t = 0ull, t_prev = 0ull;
   uint32_t e = 0u, E = 0u;
   int status = 0;
-  unsigned long long myV = 0, myD = 0, myM = 0;
+  unsigned long long myV = 0, myD = 0, myM = 0, myL = 0;  // myL: live visits (rows read)
 
   const uint32_t gl = lane & (P - 1);
   const uint32_t gmask = (P == 32) ? 0xFFFFFFFFu : (((1u << P) - 1u) << (lane & ~(uint32_t)(P - 1)));
@@ -546,6 +546,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             if (gl == 0) {
               myV += nfree;
               myD += nfree ? 1u : 0u;
+              myL += nlive;
             }
             const uint32_t rc_event = rc;
             if (nlive != 0u && !hv_loaded) {
@@ -1183,6 +1184,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             myV += nfree;
             myD += nfree ? 1u : 0u;
           }
+          if (gl == 0) myL += nlive;
           if (nlive == 0u) continue;
           // rank of slot j = #{i : key_i < key_j or (key_i == key_j and i < j)}; non-live keys
           // (~0, above every live key: w < 2^32 - 1 is enforced on the host) rank last
@@ -1299,6 +1301,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             myV += nfree;
             myD += nfree ? 1u : 0u;
           }
+          if (gl == 0) myL += nlive;
           if (nlive == 0u) continue;
           uint32_t rk[kRegDeg];
 #pragma unroll
@@ -1459,6 +1462,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             myV += nfree;
             myD += nfree ? 1u : 0u;
           }
+          if (gl == 0) myL += nlive;
           if (nlive == 0u) continue;
           // ranks among live in-links by (w, u_ord, position); positions ascend with link id.
           // Non-live keys are ~0 > every live key (w < 2^32 - 1 is enforced on the host).
@@ -1557,6 +1561,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           myV += nfree;
           myD += nfree ? 1u : 0u;
         }
+        if (gl == 0) myL += nl;
         if (nl == 0u) continue;
         if constexpr (P == 1) {
           // one lane per destination: the walk takes the live in-links in shorter-link-first order
@@ -1703,10 +1708,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   myV = warp_sum_u64(myV);
   myD = warp_sum_u64(myD);
   myM = warp_sum_u64(myM);
+  myL = warp_sum_u64(myL);
   if (lane == 0) {
     if (myV) atomicAdd(&s_V, myV);
     if (myD) atomicAdd(&s_D, myD);
     if (myM) atomicAdd(&s_M, myM);
+    if (myL) atomicAdd(&s_L, myL);
   }
   __syncthreads();
   if (Q > 1) {
@@ -1715,14 +1722,16 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       dsmem_st_u64(a, s_V);
       dsmem_st_u64(a + 8u, s_D);
       dsmem_st_u64(a + 16u, s_M);
+      dsmem_st_u64(a + 24u, s_L);
     }
     cluster.sync();  // also keeps every CTA's shared memory alive until the peers are done with it
     if (tid == 0 && crank == 0) {
-      s_V = s_D = s_M = 0ull;
+      s_V = s_D = s_M = s_L = 0ull;
       for (uint32_t r = 0; r < Q; ++r) {
         s_V += s_slot_cnt[r][0];
         s_D += s_slot_cnt[r][1];
         s_M += s_slot_cnt[r][2];
+        s_L += s_slot_cnt[r][3];
       }
     }
   }
@@ -1733,6 +1742,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     o.D = s_D;
     o.M = s_M;
     o.E = E;
+    o.Lv = s_L;
     o.status = status;
     o.pad = 0;
     outs[job.out_slot] = o;

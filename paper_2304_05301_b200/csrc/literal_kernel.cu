@@ -355,6 +355,7 @@ literal_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const La
     o.E = E;
     o.status = status;
     o.pad = (uint32_t)s_X;  // cancelled sends (duplicates + replaced outdated copies)
+    o.Lv = 0;
     outs[job.out_slot] = o;
   }
 }

@@ -503,7 +503,7 @@ struct tacos_plan {
   unsigned char *d_rows = nullptr, *d_links = nullptr;
   void *d_sort = nullptr;
   size_t sort_bytes = 0;
-  uint64_t *h_small = nullptr;  // pinned: per part {keys[2], stats[5]}
+  uint64_t *h_small = nullptr;  // pinned: per part kSmallWords {keys[2], stats}
   DevBuf h_small_buf;
   DevBuf stage_buf;             // pinned staging block of the plan's one H2D upload
   std::vector<DevBuf> bufs;
@@ -1025,7 +1025,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       o.rec_off = sg.add(ro.data(), ro.size() * 4);
     }
     for (int q = 0; q < 2; ++q) o.topo[q] = sg.reserve(sizeof(DevTopo));
-    o.keys = sg.reserve(8 * 8);
+    o.keys = sg.reserve(8 * kSmallWords);
     o.times_ag = sg.reserve(8 * (size_t)S);
     if (pt.rs_search) o.times_rs = sg.reserve(8 * (size_t)S);
   }
@@ -1119,7 +1119,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   CUDA_TRY(cudaMemcpyAsync(base, pl->stage_buf.p, sg.host.size(), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(pl->done, st));
   pl->h_small_buf.dev = dev;
-  pl->h_small_buf.p = pinned_pool().alloc(dev, 8 * 8 * (size_t)n_topos, &pl->h_small_buf.cls);
+  pl->h_small_buf.p = pinned_pool().alloc(dev, 8 * kSmallWords * (size_t)n_topos, &pl->h_small_buf.cls);
   if (!pl->h_small_buf.p) return fail(TACOS_E_NOMEM, "pinned allocation failed");
   pl->h_small = reinterpret_cast<uint64_t *>(pl->h_small_buf.p);
   if (sync) CUDA_TRY(cudaStreamSynchronize(st));
@@ -1151,7 +1151,7 @@ int plan_search(tacos_plan *pl, cudaStream_t st) {
 // Read keys + stats of every part (one D2H, one sync).
 int plan_read_small(tacos_plan *pl, cudaStream_t st) {
   for (size_t i = 0; i < pl->parts.size(); ++i)
-    CUDA_TRY(cudaMemcpyAsync(pl->h_small + 8 * i, pl->parts[i].d_keys, 8 * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(pl->h_small + kSmallWords * i, pl->parts[i].d_keys, 8 * kSmallWords, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return TACOS_OK;
 }
@@ -1166,7 +1166,7 @@ uint64_t sends_per_result(const tacos_plan *pl, const Part &pt) {
 int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capacity, tacos_result *res,
                    cudaStream_t st) {
   Part &pt = pl->parts[i];
-  const uint64_t *hs = pl->h_small + 8 * i;
+  const uint64_t *hs = pl->h_small + kSmallWords * i;
   const uint64_t key_ag = hs[0], key_rs = hs[1];
   const uint64_t *stats = hs + 2;
   std::memset(res, 0, sizeof(*res));
@@ -1175,6 +1175,7 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   res->matches = stats[2];
   res->events = stats[3];
   res->cancelled = stats[5];
+  res->live_visits = stats[6];
   res->best_key_ag = key_ag;
   res->best_key_rs = key_rs;
   const int32_t st_status = (int32_t)(int64_t)stats[4];
@@ -1344,6 +1345,8 @@ extern "C" int tacos_plan_stats(tacos_plan *pl, tacos_result *result, void *stre
   result->matches = hs[4];
   result->events = hs[5];
   result->status = (int32_t)(int64_t)hs[6];
+  result->cancelled = hs[7];
+  result->live_visits = hs[8];
   result->best_key_ag = hs[0];
   result->best_key_rs = hs[1];
   return TACOS_OK;
@@ -1677,13 +1680,14 @@ int synth_sharded(const tacos_topology *topo, const tacos_synth_params *p, uint3
   for (uint32_t g = 0; g < G; ++g)
     if (outs[g].rc) return fail(outs[g].rc, "device %u: %s", g, outs[g].err.c_str());
   tacos_result res = outs[0].res;
-  res.visits = res.dest_events = res.matches = res.events = res.cancelled = res.n_sends = 0;
+  res.visits = res.dest_events = res.matches = res.events = res.cancelled = res.n_sends = res.live_visits = 0;
   for (const ShardOut &o : outs) {
     res.visits += o.res.visits;
     res.dest_events += o.res.dest_events;
     res.matches += o.res.matches;
     res.events += o.res.events;
     res.cancelled += o.res.cancelled;
+    res.live_visits += o.res.live_visits;
     res.n_sends += o.res.n_sends;
   }
   res.winner_local = (p->collective == TACOS_ALL_REDUCE) ? 3u : (coll_need_ag(p->collective) ? 1u : 2u);

@@ -59,9 +59,11 @@ constexpr uint32_t kTraceWords = 17;  // t, delivered, t_next, matches, 8 phase 
 
 struct JobOut {
   uint64_t T, V, D, M, E;
+  uint64_t Lv;  // live visits: free links whose candidate row was read (the others were skipped exactly)
   int32_t status;
   uint32_t pad;
 };
+constexpr uint32_t kSmallWords = 16;  // per part: keys[2], stats {V, D, M, E, status, X, Lv}
 
 // Byte offsets of the per-block arrays, either in dynamic shared memory or in
 // the job's global scratch (rows / links regions).

@@ -169,11 +169,11 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
                                  unsigned long long *times_rs) {
   // per-thread partials -> warp shuffles -> one slot per warp -> warp 0 (64-bit shared
   // atomics would be CAS loops on sm_100a)
-  constexpr int kVals = 7;  // k0, k1 (min); V, D, M, E, X (sum)
+  constexpr int kVals = 8;  // k0, k1 (min); V, D, M, E, X, Lv (sum)
   __shared__ unsigned long long s_w[32][kVals];
   __shared__ int s_st[32];
   const uint32_t n_jobs = has_rs ? rs_base + n_seeds : n_seeds;
-  unsigned long long v[kVals] = {kNoKey, kNoKey, 0ull, 0ull, 0ull, 0ull, 0ull};
+  unsigned long long v[kVals] = {kNoKey, kNoKey, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
   int st = 0;
   for (uint32_t j = threadIdx.x; j < n_jobs; j += blockDim.x) {
     const JobOut o = outs[j];
@@ -182,6 +182,7 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
     v[4] += o.M;
     v[5] += o.E;
     v[6] += o.pad;
+    v[7] += o.Lv;
     if (o.status != 0) st = min(st, o.status);
     const bool is_rs = has_rs && j >= rs_base;
     const uint32_t i = is_rs ? j - rs_base : j;
@@ -225,6 +226,7 @@ __global__ void best_keys_kernel(const JobOut *__restrict__ outs, uint32_t n_see
     stats[3] = v[5];
     stats[4] = (unsigned long long)(long long)st;
     stats[5] = v[6];
+    stats[6] = v[7];
   }
 }
 
