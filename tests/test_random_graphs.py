@@ -208,3 +208,48 @@ def test_oracle_inversion_on_random_graphs(inst, seeds):
     ag0["t_end"] -= np.uint64(syn.T_rs)
     rep2 = check(n, topo.src, topo.dst, w, ag0, *ag_sets(n, k))
     assert clean(rep2), {a: b[:5] for a, b in rep2.items() if a != "T"}
+
+
+@st.composite
+def wide_instances(draw):
+    """Random graphs for the windowed loop: in-degree <= 8 (register path), C = N k >= 1025
+    chunks (more than two lanes per row), several link costs, random window cut."""
+    n = draw(st.integers(3, 12))
+    n_links = draw(st.integers(n, min(n * (n - 1), 3 * n)))
+    gseed = draw(st.integers(0, 2**31 - 1))
+    alphas = tuple(draw(st.lists(st.integers(0, 30000), min_size=1, max_size=6)))
+    bws = tuple(draw(st.lists(st.sampled_from([25, 50, 100, 200]), min_size=1, max_size=3)))
+    topo = W.random_strongly_connected(n, n_links, gseed, bws=bws, alphas=alphas)
+    k = -(-1025 // n) + draw(st.integers(0, 40))
+    seed = draw(st.integers(0, 2**40))
+    win_ev = draw(st.sampled_from(["1", "3", "256"]))
+    return topo, k, seed, win_ev
+
+
+@pytest.mark.gpu
+@settings(max_examples=40, deadline=None, derandomize=True, suppress_health_check=[HealthCheck.too_slow,
+                                                                HealthCheck.function_scoped_fixture])
+@given(wide_instances(), st.sampled_from(["AG", "RS", "AR"]), st.integers(1, 4))
+def test_gpu_windowed_loop_parity_on_random_graphs(T, inst, coll, seeds):
+    """The windowed event loop (several link costs, wide rows) against the oracle on random
+    graphs, bit-exact, with windows cut after 1, 3 or 256 events."""
+    import os
+
+    from test_gpu_parity import assert_parity
+
+    topo, k, base, win_ev = inst
+    if np.bincount(topo.dst, minlength=topo.n_npus).max() > 8:
+        return
+    nbytes = 64 << 10
+    syn = oracle.synthesize(topo, k, nbytes, coll, [base + s for s in range(seeds)])
+    t = T.Topology.from_workload_topology(topo)
+    old = os.environ.get("TACOS_WIN_EV")
+    os.environ["TACOS_WIN_EV"] = win_ev
+    try:
+        sch = T.synthesize(t, coll, k, nbytes, seeds, base, keep_seed_times=True)
+    finally:
+        if old is None:
+            os.environ.pop("TACOS_WIN_EV", None)
+        else:
+            os.environ["TACOS_WIN_EV"] = old
+    assert_parity(syn, sch, coll)
