@@ -223,12 +223,13 @@ def algorithmic_bytes(stats: dict, n_chunks: int) -> int:
 
 
 def touched_bytes(stats: dict, n_chunks: int) -> int:
-    """B with the exact skip: a free link whose source is unchanged since its last empty visit
-    has no candidates and needs no row (16 B of link state); only the Lv live visits read the
-    source row: Lv (R + 16) + (V - Lv) 16 + D (2R) + 48 M."""
+    """What the kernels move given the exact skip: a live visit reads the source row and the
+    destination's have row (2R) plus 16 B of link state, a skipped visit (source unchanged since
+    the link's last empty visit: provably no candidate) only the 16 B, a match 48 B (record +
+    arrival): Lv (2R + 16) + (V - Lv) 16 + 48 M, Lv = live visits counted by the kernels."""
     R = n_chunks / 8.0
     lv = stats.get("live_visits", stats["visits"])
-    return int(lv * (R + 16) + (stats["visits"] - lv) * 16 + stats["dest_events"] * 2 * R + 48 * stats["matches"])
+    return int(lv * (2 * R + 16) + (stats["visits"] - lv) * 16 + 48 * stats["matches"])
 
 
 def run_gpu(args):
@@ -318,10 +319,11 @@ def run_gpu(args):
     # roofline of the dominant kernel (greedy search): algorithmic bytes / kernel time, against
     # the memory level that serves them: shared memory when the plan keeps the
     # per-seed bitsets on chip (configs 1-3, 5), else HBM (config 4; L2-resident below 126 MB)
-    B_survey = algorithmic_bytes(stats, C)
-    B = touched_bytes(stats, C)
+    B = algorithmic_bytes(stats, C)
+    B_touched = touched_bytes(stats, C)
     search_avg_s = sum(search_ms) / len(search_ms) / 1e3
     achieved = B / search_avg_s / 1e9
+    touched_gbs = B_touched / search_avg_s / 1e9
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -351,8 +353,10 @@ def run_gpu(args):
         "bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "kernel": "greedy_kernel (+best_keys)", "peak_source": peak_src,
         "algorithmic_bytes_per_launch": B,
-        "bytes_definition": "Lv (R+16) + (V-Lv) 16 + D 2R + 48 M (SURVEY 8(d) B with the exact skip; Lv = live visits)",
-        "survey_bytes_per_launch": B_survey,
+        "bytes_definition": "SURVEY 8(d): V (R+16) + D 2R + 48 M, R = C/8",
+        "touched_bytes_per_launch": B_touched,
+        "touched_definition": "Lv (2R+16) + (V-Lv) 16 + 48 M (rows read given the exact skip; Lv = live visits)",
+        "frac_touched": touched_gbs / peak,
         "frac_alg_bytes_vs_hbm": achieved / hbm_peak,
         "dram_frac_of_hbm": (traffic / search_avg_s / 1e9 / hbm_peak) if traffic else None,
         "smem_pipe_frac": ncu.get("smem_pipe_frac"), "issue_active_pct": ncu.get("issue_active_pct"),

@@ -430,3 +430,13 @@ def test_windowed_loop_equals_per_event_loop(T, monkeypatch):
     b = T.synthesize(t, coll, k, 128 << 10, seeds, keep_seed_times=True)
     assert a.sends.tobytes() == b.sends.tobytes() and a.result == b.result
     assert np.array_equal(a.seed_times, b.seed_times)
+
+
+def test_large_fully_connected_uniform_rs_emission(T):
+    """FC(450): L = 202,050 links, beyond 2^16 (link state and ids in global memory) and past
+    the 48 KB default shared memory of the uniform RS emitter (2 bits per link = 49.4 KB,
+    opt-in attribute); one event, every NPU receives 449 chunks at t = 0 (P5)."""
+    topo = W.fully_connected(450)
+    syn, sch, _ = run_both(T, topo, 1, 1 << 20, "AR", 2)
+    assert_parity(syn, sch, "AR")
+    assert sch.result["T_ag"] == oracle.link_cost(500, 100, 1 << 20)
