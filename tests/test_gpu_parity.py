@@ -440,3 +440,23 @@ def test_large_fully_connected_uniform_rs_emission(T):
     syn, sch, _ = run_both(T, topo, 1, 1 << 20, "AR", 2)
     assert_parity(syn, sch, "AR")
     assert sch.result["T_ag"] == oracle.link_cost(500, 100, 1 << 20)
+
+
+def test_windowed_loop_custom_pre_post(T):
+    """The windowed loop on a CUSTOM pre/post (no relays): a hetero 12 x 12 mesh, C = 2,048
+    chunks each held by one or two random NPUs (0 to ~30 per NPU), every NPU requiring every
+    chunk (without relays a chunk only moves toward NPUs that require it, R17), so the
+    per-destination record ranges |post - pre| differ."""
+    topo = W.mesh2d(12, 12, 200, 100)
+    n, C = topo.n_npus, 2048
+    rng = np.random.default_rng(7)
+    pre_s, post_s = {}, {}
+    for c in range(C):
+        for x in rng.choice(n, int(rng.integers(1, 3)), replace=False).tolist():
+            pre_s.setdefault(x, []).append(c)
+    for x in range(n):
+        post_s[x] = list(range(C))
+    pre = oracle.bits_from_sets(n, C, pre_s)
+    post = oracle.bits_from_sets(n, C, post_s)
+    syn, sch, _ = run_both(T, topo, 1, 64 << 10, "CUSTOM", 3, pre=pre, post=post, n_chunks=C)
+    assert_parity(syn, sch, "CUSTOM")
