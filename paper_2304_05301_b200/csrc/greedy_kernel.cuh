@@ -607,14 +607,17 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                   cv[v].w &= comp == 3u ? nb : ~0u;
                 }
               }
-              // per-vector totals over the group (one reduction each); the lane scan is done for
-              // the selected vector only
-              uint32_t cnt[V], tot[V], K = 0;
+              uint32_t incl[V], tot[V], K = 0;
 #pragma unroll
               for (int v = 0; v < V; ++v) {
                 cv[v] = andnot4(cv[v], hv[v]);  // held[src](t_k) & ~have[d]
-                cnt[v] = popc4(cv[v]);
-                tot[v] = __reduce_add_sync(gmask, cnt[v]);
+                incl[v] = popc4(cv[v]);
+#pragma unroll
+                for (int o = 1; o < P; o <<= 1) {
+                  const uint32_t y = __shfl_up_sync(gmask, incl[v], o, P);
+                  if (gl >= (uint32_t)o) incl[v] += y;
+                }
+                tot[v] = __shfl_sync(gmask, incl[v], P - 1, P);
                 K += tot[v];
               }
               const uint32_t osl = jj / P;  // slot of the in-link on its owner lane
@@ -636,16 +639,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                 vsel = adv ? v + 1 : vsel;
               }
               uint4 x = cv[0];
-              uint32_t inc = cnt[0];
+              uint32_t inc = incl[0];
 #pragma unroll
               for (int v = 1; v < V; ++v) {
                 x = (vsel == v) ? cv[v] : x;
-                inc = (vsel == v) ? cnt[v] : inc;
-              }
-#pragma unroll
-              for (int o = 1; o < P; o <<= 1) {  // inclusive scan of the lane counts of vector vsel
-                const uint32_t y = __shfl_up_sync(gmask, inc, o, P);
-                if (gl >= (uint32_t)o) inc += y;
+                inc = (vsel == v) ? incl[v] : inc;
               }
               const uint32_t cx = __popc(x.x), cy = __popc(x.y), cz = __popc(x.z);
               const uint32_t excl = inc - (cx + cy + cz + __popc(x.w));
