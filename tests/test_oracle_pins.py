@@ -569,3 +569,24 @@ def test_literal_never_beats_exhaustive_optimum(inst):
     for seed in range(8):
         r = oracle.greedy(n, topo.src, topo.dst, w, n, 1, seed, literal=True)
         assert r.T >= t_opt
+
+
+def test_best_of_s_bookkeeping_r24():
+    """Reading R24: per-seed collective times and searched jobs.  Symmetric graph: one search
+    per seed, T_AR(s) = 2 T_AG(s).  Asymmetric graph: AR searches G and G^T per seed,
+    T_AR(s) = T_RS(s) + T_AG(s), the winners are chosen independently (T_AR = min T_RS +
+    min T_AG, P:L274 / R9 / R10); an RS alone searches only G^T."""
+    seeds = [0, 1, 2, 3, 4]
+    sym = oracle.synthesize(W.torus([3, 4]), 1, 1 << 20, "AR", seeds)
+    assert sym.rs is sym.ag and len(sym.ag) == 5
+    assert [int(x) for x in sym.seed_times] == [2 * g.T for g in sym.ag]
+    topo = W.random_strongly_connected(8, 19, 4, bws=(25, 50, 100), alphas=(0, 500))
+    ar = oracle.synthesize(topo, 2, 1 << 20, "AR", seeds)
+    assert ar.rs is not ar.ag and len(ar.ag) == len(ar.rs) == 5
+    assert all(g.sigma == 0 for g in ar.ag) and all(g.sigma == 1 for g in ar.rs)
+    assert [int(x) for x in ar.seed_times] == [r.T + g.T for r, g in zip(ar.rs, ar.ag)]
+    assert ar.T == min(r.T for r in ar.rs) + min(g.T for g in ar.ag)
+    rs = oracle.synthesize(topo, 2, 1 << 20, "RS", seeds)
+    assert rs.ag == [] and len(rs.rs) == 5 and all(r.sigma == 1 for r in rs.rs)
+    assert [int(x) for x in rs.seed_times] == [r.T for r in ar.rs]
+    assert rs.T == min(r.T for r in ar.rs)
