@@ -283,14 +283,20 @@ def run_gpu(args):
         torch.cuda.synchronize()
 
     def step(ev):
+        # search -> (key all-reduce) -> emission queued back to back; the winner is resolved on
+        # the device where the plan allows it, and the host reads the result after the step
         with torch.cuda.stream(stream):
             ev[0].record(stream)
             plan.search(sh)
             ev[1].record(stream)
             if world > 1:
                 plan.allreduce_keys(comm, sh)
-            res = plan.emit(d_sends.data_ptr(), n_sends, sh)
-            ev[2].record(stream)
+            if plan.emit_async(d_sends.data_ptr(), n_sends, sh):
+                ev[2].record(stream)
+                res = plan.result(n_sends, sh)
+            else:
+                res = plan.emit(d_sends.data_ptr(), n_sends, sh)
+                ev[2].record(stream)
         return res
 
     launches_per_step = None

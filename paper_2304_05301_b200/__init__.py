@@ -158,6 +158,8 @@ SIGNATURES = {
     "tacos_plan_best_keys": (_VP, [_VP]),
     "tacos_plan_emit": (ctypes.c_int, [_VP, _VP, ctypes.c_uint64, ctypes.POINTER(tacos_result), _VP]),
     "tacos_plan_seed_times_device": (_VP, [_VP, ctypes.POINTER(_VP)]),
+    "tacos_plan_emit_async": (ctypes.c_int, [_VP, _VP, ctypes.c_uint64, _VP]),
+    "tacos_plan_result": (ctypes.c_int, [_VP, ctypes.c_uint64, ctypes.POINTER(tacos_result), _VP]),
     "tacos_select_winner": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int32, ctypes.c_int,
                                            ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(tacos_winner)]),
     "tacos_plan_last_launches": (ctypes.c_uint32, [_VP]),
@@ -512,6 +514,21 @@ class Plan:
         res = tacos_result()
         _check(load_library().tacos_plan_emit(self.handle, ctypes.c_void_p(sends_ptr), capacity, ctypes.byref(res),
                                               ctypes.c_void_p(stream)), "tacos_plan_emit")
+        return res.as_dict()
+
+    def emit_async(self, sends_ptr: int, capacity: int, stream: int = 0) -> bool:
+        """tacos_plan_emit_async; False when this plan needs tacos_plan_emit instead."""
+        rc = load_library().tacos_plan_emit_async(self.handle, ctypes.c_void_p(sends_ptr), capacity,
+                                                   ctypes.c_void_p(stream))
+        if rc == TACOS_E_INVALID_ARG:
+            return False
+        _check(rc, "tacos_plan_emit_async")
+        return True
+
+    def result(self, capacity: int, stream: int = 0) -> dict:
+        res = tacos_result()
+        _check(load_library().tacos_plan_result(self.handle, capacity, ctypes.byref(res), ctypes.c_void_p(stream)),
+               "tacos_plan_result")
         return res.as_dict()
 
     def stats(self, stream: int = 0) -> dict:

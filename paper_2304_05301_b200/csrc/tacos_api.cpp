@@ -1162,9 +1162,52 @@ uint64_t sends_per_result(const tacos_plan *pl, const Part &pt) {
   return pl->p.collective == TACOS_ALL_REDUCE ? 2 * pt.cap : pt.cap;
 }
 
+// Emission that follows the search on the stream without a host round trip: the emitters
+// read the best keys on the device (DevWin).  For one part, no relays, not the literal or the
+// windowed loop (their records need a sort whose pass count depends on T), AG-type, or an
+// RS-type phase on a symmetric graph with one link cost (the sort-free mirror).  The host
+// decodes the keys afterwards (plan_emit_part with dev_launched).
+bool dev_emit_eligible(const tacos_plan *pl) {
+  if (pl->parts.size() != 1) return false;
+  const Part &pt = pl->parts[0];
+  if (pl->p.flags & (TACOS_FLAG_NO_SCHEDULE | TACOS_FLAG_LITERAL)) return false;
+  if (coll_relay(&pl->p) || pt.windowed || pt.d_rec == nullptr) return false;
+  if (coll_need_rs(pl->p.collective)) {
+    if (!pt.symmetric || pt.w.empty() || (size_t)8 * ((pt.L + 31u) / 32u) > (size_t)200 * 1024) return false;
+    for (uint32_t x : pt.w)
+      if (x != pt.w[0]) return false;
+  }
+  return true;
+}
+
+int plan_emit_dev_launch(tacos_plan *pl, tacos_send *d_sends, uint64_t capacity, cudaStream_t st) {
+  Part &pt = pl->parts[0];
+  const uint64_t nsend = sends_per_result(pl, pt);
+  if (nsend == 0 || capacity < nsend) return TACOS_OK;  // (the capacity error is raised by plan_emit_part)
+  const int coll = pl->p.collective;
+  DevWin dw{reinterpret_cast<const unsigned long long *>(pt.d_keys), pt.d_rec, pt.cap, pl->p.seed_offset,
+            pl->p.n_seeds, coll == TACOS_ALL_REDUCE ? 1u : 0u};
+  const uint64_t M = pt.required;
+  int rc;
+  if (coll_need_rs(coll)) {
+    uint32_t nl = 0;
+    if ((rc = launch_rs_uniform_emit(nullptr, M, pt.td->d_src, pt.td->d_dst, pt.w[0], pt.td->d_rev, 0, pt.L, d_sends,
+                                     pl->d_sort, pl->sort_bytes, &nl, st, &dw)))
+      return fail(rc, "%s", cuda_error_string());
+    pl->last_launches += nl;
+  }
+  if (coll_need_ag(coll)) {
+    const uint64_t base = coll == TACOS_ALL_REDUCE ? M : 0;
+    if ((rc = launch_emit_ag(nullptr, M, pt.td->d_src, pt.td->d_dst, pt.d_w, 0, d_sends + base, st, ~0ull, &dw)))
+      return fail(rc, "%s", cuda_error_string());
+    pl->last_launches += 1;
+  }
+  return TACOS_OK;
+}
+
 // Emit part i's schedule into device memory d_sends; fill res from the keys in h_small.
 int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capacity, tacos_result *res,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool dev_launched = false) {
   Part &pt = pl->parts[i];
   const uint64_t *hs = pl->h_small + kSmallWords * i;
   const uint64_t key_ag = hs[0], key_rs = hs[1];
@@ -1204,6 +1247,10 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
   const uint64_t nsend = sends_per_result(pl, pt);
   if (nsend == 0) return TACOS_OK;
   if (capacity < nsend) return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)capacity, (unsigned long long)nsend);
+  if (dev_launched) {  // emitted by plan_emit_dev_launch, winner resolved on the device
+    res->n_sends = (need_rs && rs_local ? pt.required : 0) + (need_ag && ag_local ? pt.required : 0);
+    return TACOS_OK;
+  }
   int rc;
   uint64_t emitted = 0;
   // matches of a winning job: `required` without relays, else read back from its JobOut
@@ -1326,12 +1373,36 @@ extern "C" int tacos_plan_emit(tacos_plan *pl, tacos_send *d_sends, uint64_t cap
                                void *stream) {
   if (!pl || !result) return fail(TACOS_E_INVALID_ARG, "null argument");
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = plan_read_small(pl, st);
-  if (rc) return rc;
   pl->last_launches = 0;
-  rc = plan_emit_part(pl, 0, d_sends, capacity, result, st);
+  const bool dev = dev_emit_eligible(pl) && d_sends != nullptr;
+  int rc = dev ? plan_emit_dev_launch(pl, d_sends, capacity, st) : TACOS_OK;
+  if (rc) return rc;
+  if ((rc = plan_read_small(pl, st))) return rc;
+  rc = plan_emit_part(pl, 0, d_sends, capacity, result, st, dev);
   cudaEventRecord(pl->done, st);
   return rc;
+}
+
+extern "C" int tacos_plan_emit_async(tacos_plan *pl, tacos_send *d_sends, uint64_t capacity, void *stream) {
+  if (!pl || !d_sends) return fail(TACOS_E_INVALID_ARG, "null argument");
+  if (!dev_emit_eligible(pl)) return fail(TACOS_E_INVALID_ARG, "this plan's emission needs the keys on the host (tacos_plan_emit)");
+  if (capacity < sends_per_result(pl, pl->parts[0]))
+    return fail(TACOS_E_CAPACITY, "capacity %llu < %llu sends", (unsigned long long)capacity,
+                (unsigned long long)sends_per_result(pl, pl->parts[0]));
+  cudaStream_t st = (cudaStream_t)stream;
+  pl->last_launches = 0;
+  int rc = plan_emit_dev_launch(pl, d_sends, capacity, st);
+  cudaEventRecord(pl->done, st);
+  return rc;
+}
+
+extern "C" int tacos_plan_result(tacos_plan *pl, uint64_t capacity, tacos_result *result, void *stream) {
+  if (!pl || !result) return fail(TACOS_E_INVALID_ARG, "null argument");
+  if (!dev_emit_eligible(pl)) return fail(TACOS_E_INVALID_ARG, "not a device-resolved emission (tacos_plan_emit)");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = plan_read_small(pl, st);
+  if (rc) return rc;
+  return plan_emit_part(pl, 0, nullptr, capacity, result, st, true);
 }
 
 extern "C" int tacos_plan_stats(tacos_plan *pl, tacos_result *result, void *stream) {
@@ -1463,6 +1534,40 @@ int read_seed_times_async(const Part &pt, uint32_t S, std::vector<uint64_t> &t_a
   return TACOS_OK;
 }
 
+// One part, emission resolved on the device: search, emission, D2H of the schedule (host
+// destination), keys and seed times are all queued on the stream, then one synchronization.
+int synth_one_dev(tacos_plan *pl, tacos_send *dst, tacos_result *res, std::vector<uint64_t> *seed_times,
+                  cudaStream_t st) {
+  const Part &pt = pl->parts[0];
+  const uint64_t need = sends_per_result(pl, pt);
+  const bool dev_out = need > 0 && is_device_ptr(dst);
+  tacos_send *d_out = dev_out ? dst : nullptr;
+  DevBuf tmp;
+  if (need > 0 && !dev_out) {
+    tmp.dev = pl->device;
+    tmp.p = device_pool().alloc(pl->device, need * sizeof(tacos_send), &tmp.cls);
+    if (!tmp.p) return fail(TACOS_E_NOMEM, "device allocation failed");
+    d_out = reinterpret_cast<tacos_send *>(tmp.p);
+  }
+  int rc = plan_emit_dev_launch(pl, d_out, need, st);
+  // the whole schedule (the winner is always local on one device; a failed search writes nothing)
+  if (rc == TACOS_OK && need > 0 && !dev_out) {
+    cudaError_t e = cudaMemcpyAsync(dst, d_out, need * sizeof(tacos_send), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = fail(TACOS_E_CUDA, "D2H of the schedule: %s", cudaGetErrorString(e));
+  }
+  std::vector<uint64_t> t_ag, t_rs;
+  if (rc == TACOS_OK && seed_times) rc = read_seed_times_async(pt, pl->p.n_seeds, t_ag, t_rs, st);
+  if (rc == TACOS_OK) rc = plan_read_small(pl, st);  // one synchronization for all of it
+  if (rc == TACOS_OK) rc = plan_emit_part(pl, 0, d_out, need, res, st, true);
+  if (tmp.p) device_pool().release(tmp.dev, tmp.p, tmp.cls);
+  if (rc) return rc;
+  if (seed_times) {
+    seed_times[0].resize(pl->p.n_seeds);
+    combine_seed_times(pt, pl->p.collective, pl->p.n_seeds, t_ag, t_rs, seed_times[0].data());
+  }
+  return TACOS_OK;
+}
+
 int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos_synth_params *p, tacos_send **dst,
                const uint64_t *caps, tacos_result *results, std::vector<uint64_t> *seed_times, cudaStream_t st) {
   tacos_plan *raw = nullptr;
@@ -1485,6 +1590,8 @@ int synth_many(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       fclose(f);
     }
   }
+  if (dev_emit_eligible(pl.get()) && caps[0] >= sends_per_result(pl.get(), pl->parts[0]))
+    return synth_one_dev(pl.get(), dst[0], results, seed_times, st);
   if ((rc = plan_read_small(pl.get(), st))) return rc;
   for (uint32_t i = 0; i < n_topos; ++i) {
     const Part &pt = pl->parts[i];

@@ -106,8 +106,17 @@ int launch_greedy(const Layout &lay, uint32_t P, uint32_t VPL, const Job *d_jobs
 int launch_best_keys(const JobOut *d_outs, uint32_t n_seeds, uint32_t seed_offset, uint32_t rs_base,
                      uint32_t has_rs, uint64_t *d_keys, uint64_t *d_stats, uint64_t *d_times_ag,
                      uint64_t *d_times_rs, void *stream);
+// Winner resolved on the device from the (possibly all-reduced) best keys, so the emitters
+// can follow the search without a host round trip: keys == nullptr = the host passed rec / T.
+struct DevWin {
+  const unsigned long long *keys;  // keys[0]: (T << 20) | global seed index
+  const Rec *rec_base;             // records of job 0 of the plan part
+  uint64_t cap;                    // records per job
+  uint32_t seed_offset, n_seeds;   // the shard's global seed range
+  uint32_t shift_by_T;             // emit_ag: shift the sends by the key's T (AR on a symmetric graph)
+};
 int launch_emit_ag(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
-                   uint64_t shift, void *out_sends, void *stream, uint64_t limit = ~0ull);
+                   uint64_t shift, void *out_sends, void *stream, uint64_t limit = ~0ull, const DevWin *dw = nullptr);
 int launch_compact_sends(void *sends, uint64_t n, unsigned long long *d_count, void *stream);
 int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
                         const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
@@ -115,7 +124,7 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
                         uint64_t shift = 0);
 int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, uint32_t w0,
                            const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
-                           size_t scratch_bytes, uint32_t *launches, void *stream);
+                           size_t scratch_bytes, uint32_t *launches, void *stream, const DevWin *dw = nullptr);
 int launch_literal(const Layout &lay, uint32_t VPL, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, void *stream);
 size_t rs_sort_scratch_bytes(uint64_t M);
 int launch_philox_probe(const uint32_t *d_in, uint32_t *d_out, void *stream);

@@ -250,9 +250,26 @@ struct Send32 {
 
 // limit: a send ending after it (a relay still in flight when the postcondition
 // holds, R22) is written as a tombstone (chunk = kNone) for compact_sends.
+// Winner chosen on the device (DevWin): the records of the job named by the best key, the
+// shift of an AR's AG half = T of that key (a symmetric RS lasts as long as its AG), nothing
+// written when the winning seed is not in this plan's shard.
+__device__ __forceinline__ const Rec *dev_winner(const DevWin &dw, uint64_t &T) {
+  const unsigned long long key = dw.keys[0];
+  const uint64_t g = key & ((1ull << kKeySeedBits) - 1ull);
+  T = key >> kKeySeedBits;
+  if (key == kNoKey || g < dw.seed_offset || g - dw.seed_offset >= dw.n_seeds) return nullptr;
+  return dw.rec_base + (g - dw.seed_offset) * dw.cap;
+}
+
 __global__ void emit_ag_kernel(const Rec *__restrict__ rec, uint64_t M, const uint32_t *__restrict__ src,
                                const uint32_t *__restrict__ dst, const uint32_t *__restrict__ w, uint64_t shift,
-                               uint64_t limit, Send32 *__restrict__ out) {
+                               uint64_t limit, Send32 *__restrict__ out, DevWin dw) {
+  if (dw.keys) {
+    uint64_t T;
+    rec = dev_winner(dw, T);
+    if (!rec) return;
+    shift = dw.shift_by_T ? T : 0ull;
+  }
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < M; i += (uint64_t)gridDim.x * blockDim.x) {
     const Rec r = rec[i];
     Send32 s;
@@ -274,9 +291,10 @@ static int grid_for(uint64_t n, int threads) {
 }
 
 int launch_emit_ag(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, const uint32_t *w,
-                   uint64_t shift, void *out_sends, void *stream, uint64_t limit) {
+                   uint64_t shift, void *out_sends, void *stream, uint64_t limit, const DevWin *dw) {
   emit_ag_kernel<<<grid_for(M, 256), 256, 0, (cudaStream_t)stream>>>(rec, M, src, dst, w, shift, limit,
-                                                                      reinterpret_cast<Send32 *>(out_sends));
+                                                                      reinterpret_cast<Send32 *>(out_sends),
+                                                                      dw ? *dw : DevWin{});
   return check_launch("emit_ag_kernel");
 }
 
@@ -539,7 +557,13 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
 // starts: the segment starts (unordered); flags[i] = 1 where a segment starts (i < M), 0 up to
 // the 16-byte padded end, so a CTA finds a segment's end with 16-flag vector loads
 __global__ void seg_starts_kernel(const Rec *__restrict__ rec, uint64_t M, uint32_t *__restrict__ starts,
-                                  unsigned int *__restrict__ n_seg, unsigned char *__restrict__ flags, uint64_t n_flags) {
+                                  unsigned int *__restrict__ n_seg, unsigned char *__restrict__ flags, uint64_t n_flags,
+                                  DevWin dw) {
+  if (dw.keys) {
+    uint64_t T;
+    rec = dev_winner(dw, T);
+    if (!rec) return;
+  }
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_flags; i += (uint64_t)gridDim.x * blockDim.x) {
     const bool b = i < M && (i == 0 || rec[i].t_start != rec[i - 1].t_start);
     flags[i] = b ? 1 : 0;
@@ -551,8 +575,12 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
                                        const unsigned int *__restrict__ n_seg, const unsigned char *__restrict__ flags,
                                        uint64_t n_flags, const uint32_t *__restrict__ src,
                                        const uint32_t *__restrict__ dst, uint32_t w0, const int32_t *__restrict__ rev,
-                                       uint64_t T_rs, uint32_t L, Send32 *__restrict__ out) {
+                                       uint64_t T_rs, uint32_t L, Send32 *__restrict__ out, DevWin dw) {
   extern __shared__ uint32_t sm[];
+  if (dw.keys) {
+    rec = dev_winner(dw, T_rs);
+    if (!rec) return;
+  }
   const uint32_t nbw = (L + 31u) / 32u;
   uint32_t *bm = sm, *pre = sm + nbw;
   __shared__ unsigned long long s_end;
@@ -628,7 +656,8 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
 
 int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, uint32_t w0,
                            const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
-                           size_t scratch_bytes, uint32_t *launches, void *stream) {
+                           size_t scratch_bytes, uint32_t *launches, void *stream, const DevWin *dw) {
+  const DevWin dwv = dw ? *dw : DevWin{};
   cudaStream_t st = (cudaStream_t)stream;
   if (M == 0) return 0;
   if (scratch_bytes < 256 + ((M * 4 + 255) / 256) * 256 + M + 16 || M >= (1ull << 32)) {
@@ -640,7 +669,7 @@ int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, cons
   const uint64_t n_flags = (M + 15u) & ~15ull;
   unsigned char *flags = reinterpret_cast<unsigned char *>(scratch) + 256 + ((M * 4 + 255) / 256) * 256;
   cudaMemsetAsync(n_seg, 0, sizeof(unsigned int), st);
-  seg_starts_kernel<<<grid_for(n_flags, 256), 256, 0, st>>>(rec, M, starts, n_seg, flags, n_flags);
+  seg_starts_kernel<<<grid_for(n_flags, 256), 256, 0, st>>>(rec, M, starts, n_seg, flags, n_flags, dwv);
   int rc = check_launch("seg_starts_kernel");
   if (rc) return rc;
   const uint32_t nbw = (L + 31u) / 32u;
@@ -654,7 +683,7 @@ int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, cons
     }
   }
   rs_uniform_emit_kernel<<<148, 1024, smem, st>>>(rec, M, starts, n_seg, flags, n_flags, src, dst, w0, rev, T_rs, L,
-                                                             reinterpret_cast<Send32 *>(out_sends));
+                                                   reinterpret_cast<Send32 *>(out_sends), dwv);
   if (launches) *launches += 2;
   return check_launch("rs_uniform_emit_kernel");
 }

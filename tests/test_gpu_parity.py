@@ -460,3 +460,41 @@ def test_windowed_loop_custom_pre_post(T):
     post = oracle.bits_from_sets(n, C, post_s)
     syn, sch, _ = run_both(T, topo, 1, 64 << 10, "CUSTOM", 3, pre=pre, post=post, n_chunks=C)
     assert_parity(syn, sch, "CUSTOM")
+
+
+def test_plan_emit_async_device_winner(T):
+    """tacos_plan_emit_async (winner resolved on the device, no host round trip) then
+    tacos_plan_result: the oracle's schedule and result; two seed shards whose forced keys
+    name a seed of the other shard write nothing; a windowed plan (records sorted at
+    emission) is refused and uses tacos_plan_emit."""
+    import torch
+
+    wl = W.config(3)
+    t = T.Topology.from_workload_topology(wl.topo)
+    syn = oracle.synthesize(wl.topo, 1, 1 << 20, "AR", list(range(8)))
+    st = torch.cuda.current_stream().cuda_stream
+    plans = [T.Plan(t, "AR", 1, 1 << 20, 4, 0, off) for off in (0, 4)]
+    for pl in plans:
+        pl.search(st)
+    keys = [pl.best_keys_tensor().clone() for pl in plans]
+    gmin = torch.minimum(keys[0], keys[1])
+    owners = 0
+    for pl in plans:
+        pl.best_keys_tensor().copy_(gmin)
+        out = torch.full((pl.n_sends * 32,), 0xAB, dtype=torch.uint8, device="cuda")
+        assert pl.emit_async(out.data_ptr(), pl.n_sends, st)
+        res = pl.result(pl.n_sends, st)
+        assert res["T"] == syn.T and res["seed"] == syn.seed
+        if res["winner_local"]:
+            owners += 1
+            assert res["n_sends"] == pl.n_sends
+            assert T.sends_from_bytes(out.cpu().numpy()).tobytes() == syn.sends.tobytes()
+        else:
+            assert res["n_sends"] == 0 and bool((out == 0xAB).all())
+    assert owners == 1
+    t4 = T.Topology.from_workload_topology(W.mesh2d(16, 16, 200, 100))
+    pw = T.Plan(t4, "AR", 8, 128 << 10, 2)
+    pw.search(st)
+    buf = torch.empty(pw.n_sends * 32, dtype=torch.uint8, device="cuda")
+    assert not pw.emit_async(buf.data_ptr(), pw.n_sends, st)
+    assert pw.emit(buf.data_ptr(), pw.n_sends, st)["n_sends"] == pw.n_sends
