@@ -298,17 +298,23 @@ def test_synthesize_into_host_and_device(T):
     torch.cuda.synchronize()
     assert r1["T"] == r2["T"] and r1["n_sends"] == n
     assert host.numpy().tobytes() == dev.cpu().numpy().tobytes()
+    syn = oracle.synthesize(wl.topo, 1, 1 << 20, "AR", list(range(4)))
+    assert r1["T"] == syn.T and r1["seed"] == syn.seed
+    assert host.numpy().tobytes() == syn.sends.tobytes()
     with pytest.raises(T.TacosError) as e:
         T.synthesize_into(t, p, dev.data_ptr(), n - 1)
     assert e.value.code == T.TACOS_E_CAPACITY
 
 
 def test_determinism(T):
+    """Three runs byte-identical, and equal to the oracle's."""
     wl = W.config(5)
     t = T.Topology.from_workload_topology(wl.topo)
     a = [T.synthesize(t, "AR", 1, 1 << 20, 32) for _ in range(3)]
     for b in a[1:]:
         assert b.sends.tobytes() == a[0].sends.tobytes() and b.result == a[0].result
+    syn = oracle.synthesize(wl.topo, 1, 1 << 20, "AR", list(range(32)))
+    assert a[0].sends.tobytes() == syn.sends.tobytes() and a[0].result["T"] == syn.T
 
 
 def test_paper_512_ring_fc_switch_asymmetric(T):
