@@ -1725,9 +1725,14 @@ int synth_sharded(const tacos_topology *topo, const tacos_synth_params *p, uint3
     pg.n_seeds = hi - lo;
     if (cudaSetDevice((int)g) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
       r = fail(TACOS_E_CUDA, "device %u: %s", g, cudaGetErrorString(cudaGetLastError()));
-    if (!r) r = plan_build(&topo, 1, &pg, &raw, st, false);
-    std::unique_ptr<tacos_plan> pl(raw);
-    if (!r) r = plan_search(pl.get(), st);
+    std::unique_ptr<tacos_plan> pl;
+    try {  // no exception may leave a worker thread, and every worker must reach the rendezvous
+      if (!r) r = plan_build(&topo, 1, &pg, &raw, st, false);
+      pl.reset(raw);
+      if (!r) r = plan_search(pl.get(), st);
+    } catch (...) {
+      r = TACOS_E_NOMEM;
+    }
     const bool go = rv.arrive(r != 0);
     if (go) {
       uint64_t *keys = pl->parts[0].d_keys;
@@ -1777,7 +1782,15 @@ int synth_sharded(const tacos_topology *topo, const tacos_synth_params *p, uint3
   };
   {
     std::vector<std::thread> th;
-    for (uint32_t g = 0; g < G; ++g) th.emplace_back(work, g);
+    for (uint32_t g = 0; g < G; ++g)
+      th.emplace_back([&, g] {
+        try {
+          work(g);
+        } catch (...) {  // (past the rendezvous: only host allocations can throw here)
+          outs[g].rc = TACOS_E_NOMEM;
+          outs[g].err = "host allocation failed";
+        }
+      });
     for (auto &t : th) t.join();
   }
   cudaSetDevice(caller);
@@ -1880,8 +1893,12 @@ extern "C" int tacos_synthesize_batch(const tacos_topology *const *topos, uint32
         tacos_synth_params pg = *p;
         pg.n_devices = 1;
         int r = cudaSetDevice((int)g) == cudaSuccess ? TACOS_OK : fail(TACOS_E_CUDA, "cudaSetDevice(%u)", g);
-        if (!r) r = synth_many(tg.data(), (uint32_t)tg.size(), &pg, dg.data(), cg.data(), rg.data(),
-                               keep ? tmg.data() : nullptr, nullptr);
+        try {  // no exception may leave a worker thread
+          if (!r) r = synth_many(tg.data(), (uint32_t)tg.size(), &pg, dg.data(), cg.data(), rg.data(),
+                                 keep ? tmg.data() : nullptr, nullptr);
+        } catch (...) {
+          r = fail(TACOS_E_NOMEM, "host allocation failed");
+        }
         if (!r)
           for (size_t j = 0; j < idx.size(); ++j) {
             res[idx[j]] = rg[j];
@@ -1893,7 +1910,15 @@ extern "C" int tacos_synthesize_batch(const tacos_topology *const *topos, uint32
       int caller = 0;
       cudaGetDevice(&caller);
       std::vector<std::thread> th;
-      for (uint32_t g = 0; g < G; ++g) th.emplace_back(work, g);
+      for (uint32_t g = 0; g < G; ++g)
+        th.emplace_back([&, g] {
+          try {
+            work(g);
+          } catch (...) {
+            rcs[g] = TACOS_E_NOMEM;
+            errs[g] = "host allocation failed";
+          }
+        });
       for (auto &t : th) t.join();
       cudaSetDevice(caller);
       for (uint32_t g = 0; g < G && !rc; ++g)
