@@ -335,11 +335,13 @@ def run_gpu(args):
     # roofline of the dominant kernel (greedy search): algorithmic bytes / kernel time, against
     # the memory level that serves them: shared memory when the plan keeps the
     # per-seed bitsets on chip (configs 1-3, 5), else HBM (config 4; L2-resident below 126 MB)
-    B = algorithmic_bytes(stats, C)
-    B_touched = touched_bytes(stats, C)
+    # achieved = the bytes the kernels move per launch given the exact skip; SURVEY
+    # §8(d)'s B (a row per visit, two per destination-event) is reported beside it
+    B_survey = algorithmic_bytes(stats, C)
+    B = touched_bytes(stats, C)
     search_avg_s = sum(search_ms) / len(search_ms) / 1e3
     achieved = B / search_avg_s / 1e9
-    touched_gbs = B_touched / search_avg_s / 1e9
+    survey_gbs = B_survey / search_avg_s / 1e9
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -369,11 +371,12 @@ def run_gpu(args):
         "bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "traffic": traffic, "kernel": "greedy_kernel (+best_keys)", "peak_source": peak_src,
         "algorithmic_bytes_per_launch": B,
-        "bytes_definition": "SURVEY 8(d): V (R+16) + D 2R + 48 M, R = C/8",
-        "touched_bytes_per_launch": B_touched,
-        "touched_definition": "Lv (2R+16) + (V-Lv) 16 + 48 M (rows read given the exact skip; Lv = live visits)",
-        "frac_touched": touched_gbs / peak,
-        "frac_alg_bytes_vs_hbm": achieved / hbm_peak,
+        "bytes_definition": "Lv (2R+16) + (V-Lv) 16 + 48 M, R = C/8: a live visit reads the source row and the "
+                            "destination's have row, a visit skipped exactly (source unchanged) 16 B of link state, "
+                            "a match 48 B; Lv = live visits counted by the kernels",
+        "survey_bytes_per_launch": B_survey,
+        "frac_survey_bytes": survey_gbs / peak,
+        "frac_vs_hbm": achieved / hbm_peak,
         "dram_frac_of_hbm": (traffic / search_avg_s / 1e9 / hbm_peak) if traffic else None,
         "smem_pipe_frac": ncu.get("smem_pipe_frac"), "issue_active_pct": ncu.get("issue_active_pct"),
         "warps_active_pct": ncu.get("warps_active_pct"), "ncu_source": ncu.get("source"),
