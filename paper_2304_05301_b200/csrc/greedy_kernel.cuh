@@ -188,7 +188,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       v = __ldg(&T.pre[i]);
       hv0 = MASKED ? v : (v | ~__ldg(&T.post[i]));
     } else {  // AG: chunks x*k .. x*k+k-1 (R12)
-      const uint32_t lo = x * T.k, hi = lo + T.k, wlo = q * 32u, whi = wlo + 32u;
+      const uint32_t xo = T.npu_orig ? T.npu_orig[x] : x;  // chunks of the NPU's original id (R12)
+      const uint32_t lo = xo * T.k, hi = lo + T.k, wlo = q * 32u, whi = wlo + 32u;
       const uint32_t a = lo > wlo ? lo : wlo, b = hi < whi ? hi : whi;
       v = 0u;
       if (a < b) v = ((b - a) == 32u ? 0xFFFFFFFFu : ((1u << (b - a)) - 1u)) << (a - wlo);
@@ -359,9 +360,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         w_evo[i] = 0u;
       }
       for (uint32_t i = d_lo + tid; i < d_hi; i += nthr) rcnt[i - d_lo] = 0u;
+      if (tid == 0) s_dbg[1] = ~0u;
       cluster_barrier();  // peers push into our bitmap / lists from now on
       unsigned long long delivered = 0ull;  // cluster-wide deliveries before the window
       for (;;) {
+        long long wts[9];  // debug (TACOS_TRACE): window phase timestamps, thread 0 of job 0
+        const bool wtr = job.trace != nullptr && tid == 0;
+        if (wtr) wts[0] = clock64();
         // ---- (1) event offsets of [t, t + W) ----
         for (uint32_t q = p_lo + tid; q < p_hi; q += nthr)
           if (cur[q] != kNone) {
@@ -378,31 +383,38 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
                 if (r != crank) dsmem_or_b32(dsmem_addr(&w_bm[i], r), v);
           }
         }
+        if (wtr) wts[1] = clock64();
         cluster_barrier();
+        if (wtr) wts[2] = clock64();
         // ---- (2) sorted offsets, the window limit (first offset left out) ----
+        // warp 0: lane l takes the words [l cw, (l + 1) cw) (ascending offsets lane by lane), one
+        // scan of the lane counts places every offset
         if (tid < 32) {
-          uint32_t n = 0;
-          if (lane == 0) s_wlim = Wwin;
-          for (uint32_t b = 0; b < nbm && n <= kEv; b += 32u) {
-            const uint32_t i = b + lane;
-            const uint32_t v = i < nbm ? w_bm[i] : 0u, c = __popc(v);
-            uint32_t incl = c;
+          const uint32_t cw = (nbm + 31u) / 32u, w0 = lane * cw, w1 = min(nbm, w0 + cw);
+          uint32_t c = 0;
+          for (uint32_t i = w0; i < w1; ++i) c += __popc(w_bm[i]);
+          uint32_t incl = c;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-              if (lane >= (uint32_t)o) incl += y;
-            }
-            uint32_t pos = n + incl - c;
-            for (uint32_t m = v; m; m &= m - 1u, ++pos) {
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+          }
+          const uint32_t n = __shfl_sync(0xFFFFFFFFu, incl, 31);
+          if (lane == 0) {
+            s_nev = n < kEv ? n : kEv;
+            s_wlim = Wwin;
+          }
+          __syncwarp();
+          uint32_t pos = incl - c;
+          for (uint32_t i = w0; i < w1 && pos <= kEv; ++i)
+            for (uint32_t m = w_bm[i]; m && pos <= kEv; m &= m - 1u, ++pos) {
               const uint32_t off = i * 32u + (uint32_t)(__ffs(m) - 1);
               if (pos < kEv) w_ev[pos] = off;
-              else if (pos == kEv) s_wlim = off;
+              else s_wlim = off;  // the first offset of the next window
             }
-            n += __shfl_sync(0xFFFFFFFFu, incl, 31);
-          }
-          if (lane == 0) s_nev = n < kEv ? n : kEv;
         }
         __syncthreads();
+        if (wtr) wts[3] = clock64();
         const uint32_t n_ev = s_nev, wlim = s_wlim;
         for (uint32_t i = tid; i < nbm; i += nthr) w_bm[i] = 0u;  // peers write it again after (6)
         TCHECK(n_ev >= 1u && n_ev <= kEv && kEv <= kWinEv && w_ev[0] == 0u, "window events");
@@ -450,29 +462,39 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             }
           }
         }
+        if (wtr) wts[4] = clock64();
         cluster_barrier();
+        if (wtr) wts[5] = clock64();
         // ---- (4) done test inside the window ----
-        if (tid == 0) {
+        if (tid < 32) {  // warp 0: cumulative deliveries per event (a scan per 32 events)
           unsigned long long acc = delivered;
           uint32_t kd = kNone;
-          for (uint32_t k = 0; k < n_ev; ++k) {
-            acc += w_evc[k];
-            if (acc == T.required) {
-              kd = k;
-              break;
+          for (uint32_t b = 0; b < n_ev; b += 32u) {
+            const uint32_t i = b + lane;
+            const uint32_t v = i < n_ev ? w_evc[i] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+              if (lane >= (uint32_t)o) incl += y;
             }
+            const uint32_t hit = __ballot_sync(0xFFFFFFFFu, i < n_ev && acc + incl == T.required);
+            if (hit && kd == kNone) kd = b + (uint32_t)(__ffs(hit) - 1);
+            acc += __shfl_sync(0xFFFFFFFFu, incl, 31);
           }
-          s_kdone = kd;
-          unsigned long long tot = 0;
-          for (uint32_t k = 0; k < n_ev; ++k) tot += w_evc[k];
-          s_wdel = tot;
-          s_wmin = ~0u;
-          s_wnext = 0u;
+          if (lane == 0) {
+            s_kdone = kd;
+            s_wdel = acc - delivered;
+            s_wmin = ~0u;
+            s_wnext = 0u;
+          }
         }
         __syncthreads();
         const uint32_t k_done = s_kdone;
         const uint32_t n_run = k_done == kNone ? n_ev : k_done;
         E += n_run;
+        if (wtr) wts[6] = clock64();
+        const long long g_t0 = job.trace != nullptr ? clock64() : 0;  // debug: per-group phase time
         // ---- (5) destinations: every event of the window before done ----
         constexpr int SL = (kRegDeg + P - 1) / P;
         // destinations are taken from a shared counter, one group at a time: their costs differ
@@ -694,6 +716,8 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             // the next event that can change this destination's state, and the free in-links
             // until then (this event's claims are busy now)
             const uint32_t nf = nfree - (rc - rc_event);  // every claim of this event took a free in-link
+            // (a busy in-link matters again only when it frees -- its source's state is read
+            // then -- so source arrivals count for the free in-links only)
             uint32_t nx = ~0u;
 #pragma unroll
             for (int sl = 0; sl < SL; ++sl) {
@@ -702,6 +726,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               if (bq[sl] > tk) {
                 const unsigned long long o = bq[sl] - t;
                 if (o < wlim && (uint32_t)o < nx) nx = (uint32_t)o;
+                continue;
               }
 #pragma unroll
               for (int a = 0; a < kWinReg; ++a) {
@@ -732,6 +757,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             if (gl == 0) rcnt[wi] = rc;
           }
         }
+        if (job.trace != nullptr && gl == 0) {
+          atomicMax(&s_dbg[0], (unsigned)(clock64() - g_t0));
+          atomicMin(&s_dbg[1], (unsigned)(clock64() - g_t0));
+        }
+        if (wtr) wts[7] = clock64();
         __syncthreads();
         // ---- (6) end of the window ----
         delivered += s_wdel;
@@ -773,6 +803,20 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         if (mo_all == ~0u) {  // nothing in flight and not done: stall (R17)
           status = -3;
           break;
+        }
+        if (wtr && e % job.trace_stride == 0u && e / job.trace_stride < kTraceEvents) {
+          wts[8] = clock64();
+          unsigned long long *tr = job.trace + ((size_t)crank * kTraceEvents + e / job.trace_stride) * kTraceWords;
+          tr[0] = t;
+          tr[1] = n_ev;
+          tr[2] = n_run;
+          tr[3] = wlim;
+          for (int i = 1; i < 9; ++i) tr[3 + i] = (unsigned long long)(wts[i] - wts[i - 1]);
+          tr[12] = s_dbg[0];  // slowest group's destination phase
+          tr[13] = s_dbg[1];  // fastest group's
+          tr[14] = tr[15] = tr[16] = 0;
+          s_dbg[0] = 0u;
+          s_dbg[1] = ~0u;
         }
         t += mo_all;
         if (t >= kMaxTime) {

@@ -978,6 +978,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
   const size_t o_outs = sg.reserve(sizeof(JobOut) * n_jobs), o_count = sg.reserve(8);
   struct PartOffs {
     size_t w, pos_w[2], allow[2] = {0, 0}, pre = 0, post = 0, topo[2], keys, times_ag, times_rs = 0, rec_off = 0;
+    size_t orig = 0, in_ptr[2] = {0, 0}, pos_lid[2] = {0, 0}, pos_src[2] = {0, 0}, pos_dst[2] = {0, 0};
+    bool relabel = false;
   };
   std::vector<PartOffs> po(n_topos);
   for (uint32_t i = 0; i < n_topos; ++i) {
@@ -985,11 +987,58 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     const tacos_topology *t = pt.topo;
     PartOffs &o = po[i];
     o.w = sg.add(pt.w.data(), pt.w.size() * 4);
-    for (int q = 0; q < 2; ++q) {  // per-position costs of both orientations
-      std::vector<uint32_t> pw(pt.L);
-      for (uint32_t x = 0; x < pt.L; ++x) pw[x] = pt.w[t->pos_lid[q][x]];
-      o.pos_w[q] = sg.add(pw.data(), pw.size() * 4);
+    // Windowed parts on a cluster: NPUs relabeled so that each CTA's contiguous block of kernel
+    // ids holds several id blocks spread over the topology (block b of ~N / (Q m) ids goes to CTA
+    // b mod Q), balancing the CTAs of a cluster (a CTA of border NPUs was the slowest).  The result
+    // is unchanged: chunk ids (the AG init reads the original id), link ids, the Philox counters
+    // and the in-link order of every NPU stay the same; records carry link ids.
+    std::vector<uint32_t> orig;  // kernel id -> original id
+    uint32_t Qg = 1;
+    for (const Group &g : pl->groups)
+      if (pt.job_base >= g.job_begin && pt.job_base < g.job_end) Qg = g.lay.cluster ? g.lay.cluster : 1u;
+    uint32_t mil = 8;  // blocks per CTA (config 4: 249 / 235 / 233 / 231 ms at 0 (off) / 4 / 2 / 8)
+    if (const char *env = getenv("TACOS_INTERLEAVE")) mil = (uint32_t)std::max(0, atoi(env));
+    o.relabel = pt.windowed && Qg > 1 && mil > 0 && pt.N >= 2 * Qg * mil;
+    std::vector<uint32_t> newid;
+    if (o.relabel) {
+      const uint32_t nb = Qg * mil, bs = (pt.N + nb - 1) / nb;
+      orig.resize(pt.N);
+      for (uint32_t x = 0; x < pt.N; ++x) orig[x] = x;
+      std::stable_sort(orig.begin(), orig.end(), [&](uint32_t a, uint32_t b) {
+        return (a / bs) % Qg < (b / bs) % Qg || ((a / bs) % Qg == (b / bs) % Qg && a < b);
+      });
+      newid.resize(pt.N);
+      for (uint32_t x = 0; x < pt.N; ++x) newid[orig[x]] = x;
+      o.orig = sg.add(orig.data(), orig.size() * 4);
+      for (int q = 0; q < 2; ++q) {  // the CSR in kernel ids, each NPU's in-links in their original order
+        std::vector<uint32_t> ip(pt.N + 1, 0u), lid(pt.L), src(pt.L), dst(pt.L);
+        uint32_t k = 0;
+        for (uint32_t x2 = 0; x2 < pt.N; ++x2) {
+          const uint32_t x = orig[x2];
+          ip[x2] = k;
+          for (uint32_t p = t->in_ptr[q][x]; p < t->in_ptr[q][x + 1]; ++p, ++k) {
+            lid[k] = t->pos_lid[q][p];
+            src[k] = newid[t->pos_src[q][p]];
+            dst[k] = x2;
+          }
+        }
+        ip[pt.N] = k;
+        o.in_ptr[q] = sg.add(ip.data(), ip.size() * 4);
+        o.pos_lid[q] = sg.add(lid.data(), lid.size() * 4);
+        o.pos_src[q] = sg.add(src.data(), src.size() * 4);
+        o.pos_dst[q] = sg.add(dst.data(), dst.size() * 4);
+        std::vector<uint32_t> pw(pt.L);
+        for (uint32_t x = 0; x < pt.L; ++x) pw[x] = pt.w[lid[x]];
+        o.pos_w[q] = sg.add(pw.data(), pw.size() * 4);
+      }
+    } else {
+      for (int q = 0; q < 2; ++q) {  // per-position costs of both orientations
+        std::vector<uint32_t> pw(pt.L);
+        for (uint32_t x = 0; x < pt.L; ++x) pw[x] = pt.w[t->pos_lid[q][x]];
+        o.pos_w[q] = sg.add(pw.data(), pw.size() * 4);
+      }
     }
+    auto kid = [&](uint32_t x2) { return o.relabel ? orig[x2] : x2; };  // original id of kernel NPU x2
     if (relay) {
       for (int q = 0; q < 2; ++q) {
         std::vector<uint32_t> allow;
@@ -1002,8 +1051,8 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       std::vector<uint32_t> pre_p((size_t)pt.N * pt.Wp, 0u), post_p((size_t)pt.N * pt.Wp, 0u);
       for (uint32_t x = 0; x < pt.N; ++x)
         for (uint32_t q = 0; q < W0; ++q) {
-          pre_p[(size_t)x * pt.Wp + q] = pl->pre[(size_t)x * W0 + q];
-          post_p[(size_t)x * pt.Wp + q] = pl->post[(size_t)x * W0 + q];
+          pre_p[(size_t)x * pt.Wp + q] = pl->pre[(size_t)kid(x) * W0 + q];
+          post_p[(size_t)x * pt.Wp + q] = pl->post[(size_t)kid(x) * W0 + q];
         }
       o.pre = sg.add(pre_p.data(), pre_p.size() * 4);
       o.post = sg.add(post_p.data(), post_p.size() * 4);
@@ -1016,7 +1065,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         if (custom) {
           need = 0;
           for (uint32_t q = 0; q < W0; ++q)
-            need += (uint32_t)__builtin_popcount(pl->post[(size_t)x * W0 + q] & ~pl->pre[(size_t)x * W0 + q]);
+            need += (uint32_t)__builtin_popcount(pl->post[(size_t)kid(x) * W0 + q] & ~pl->pre[(size_t)kid(x) * W0 + q]);
         } else {
           need = pt.C - pt.k;
         }
@@ -1049,11 +1098,12 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       h.VPL = pt.VPL;
       h.custom = custom ? 1u : 0u;
       h.required = pt.required;
-      h.in_ptr = pt.td->d_in_ptr[q];
-      h.p_src = pt.td->d_pos_src[q];
-      h.p_dst = pt.td->d_pos_dst[q];
+      h.in_ptr = o.relabel ? reinterpret_cast<const uint32_t *>(base + o.in_ptr[q]) : pt.td->d_in_ptr[q];
+      h.p_src = o.relabel ? reinterpret_cast<const uint32_t *>(base + o.pos_src[q]) : pt.td->d_pos_src[q];
+      h.p_dst = o.relabel ? reinterpret_cast<const uint32_t *>(base + o.pos_dst[q]) : pt.td->d_pos_dst[q];
       h.p_w = reinterpret_cast<const uint32_t *>(base + o.pos_w[q]);
-      h.p_lid = pt.td->d_pos_lid[q];
+      h.p_lid = o.relabel ? reinterpret_cast<const uint32_t *>(base + o.pos_lid[q]) : pt.td->d_pos_lid[q];
+      h.npu_orig = o.relabel ? reinterpret_cast<const uint32_t *>(base + o.orig) : nullptr;
       h.pre = custom ? reinterpret_cast<const uint32_t *>(base + o.pre) : nullptr;
       h.post = custom ? reinterpret_cast<const uint32_t *>(base + o.post) : nullptr;
       h.allow = relay ? reinterpret_cast<const uint32_t *>(base + o.allow[q]) : nullptr;

@@ -32,6 +32,7 @@ struct DevTopo {
   const uint32_t *pre;    // [N*Wp] custom only
   const uint32_t *post;   // [N*Wp] custom only
   const uint32_t *allow;  // [L*Wp] relays only (R22): chunks position p may carry, else nullptr
+  const uint32_t *npu_orig;  // [N] original id of kernel NPU x when the plan relabels NPUs, else nullptr
 };
 
 // Compact send record written by the search (16 B): ordered by (t_start, link)
