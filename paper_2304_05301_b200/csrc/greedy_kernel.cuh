@@ -569,6 +569,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               myV += nfree;
               myD += nfree ? 1u : 0u;
               myL += nlive;
+              if (job.trace != nullptr) {  // debug: processed events, walked in-links
+                atomicAdd(&s_dbg[2], 1u);
+                atomicAdd(&s_dbg[3], nlive);
+              }
             }
             const uint32_t rc_event = rc;
             if (nlive != 0u && !hv_loaded) {
@@ -814,8 +818,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           for (int i = 1; i < 9; ++i) tr[3 + i] = (unsigned long long)(wts[i] - wts[i - 1]);
           tr[12] = s_dbg[0];  // slowest group's destination phase
           tr[13] = s_dbg[1];  // fastest group's
-          tr[14] = tr[15] = tr[16] = 0;
-          s_dbg[0] = 0u;
+          tr[14] = s_dbg[2];  // processed (destination, event) pairs of this CTA
+          tr[15] = s_dbg[3];  // walked in-links
+          tr[16] = 0;
+          s_dbg[0] = s_dbg[2] = s_dbg[3] = 0u;
           s_dbg[1] = ~0u;
         }
         t += mo_all;

@@ -26,4 +26,5 @@ for rank in sorted(set(x[0] for x in rows)):
     tot = [sum(x[6 + i] for x in rr) for i in range(8)]
     print(f"rank {rank}: windows {n}, events/window {sum(x[3] for x in rr) / n:.1f} (run {sum(x[4] for x in rr) / n:.1f}), "
           f"cycles/window {sum(tot) / n:.0f}: " + " ".join(f"{nm}={tot[i] / n:.0f}" for i, nm in enumerate(names)) +
-          f" | group phase max {sum(x[14] for x in rr) / n:.0f} min {sum(x[15] for x in rr) / n:.0f}")
+          f" | group phase max {sum(x[14] for x in rr) / n:.0f} min {sum(x[15] for x in rr) / n:.0f}"
+          f" | processed (dest, event) {sum(x[16] for x in rr) / n:.0f} walked links {sum(x[17] for x in rr) / n:.0f}")
