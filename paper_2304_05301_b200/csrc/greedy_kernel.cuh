@@ -50,6 +50,9 @@ constexpr bool kP1Smem = true;
 #define TACOS_P1_HAVE_REG 0
 #endif
 
+#ifndef TACOS_WIN_EAGER_HAVE  // 1: the windowed loop reads a destination's have row up front
+#define TACOS_WIN_EAGER_HAVE 0
+#endif
 #ifndef TACOS_STEP1  // 1: the P == 1 walk step keeps per-word counts and selects the bit without POPC
 #define TACOS_STEP1 1  // measured: config 2 0.283 -> 0.269 ms, config 3 0.745 -> 0.740, config 5 3.044 -> 3.015
 #endif
@@ -509,6 +512,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
           uint4 hv[V];
           bool hv_loaded = false;  // the have row (L2 with global rows) is read at the first live event
+#if TACOS_WIN_EAGER_HAVE
+#pragma unroll
+          for (int v = 0; v < V; ++v) hv[v] = have4[v * P + gl];
+          hv_loaded = true;
+#endif
+          const uint32_t rbase = rec != nullptr ? __ldg(&rec_off[d]) : 0u;  // issued early: an L2 round trip
           unsigned long long bq[SL];
           uint32_t sq[SL], srq[SL], hq[SL], nq[SL];
           // the first kWinReg window-arrival offsets of each slot's source, in registers (~0 = none)
@@ -705,12 +714,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
               if (gl == 0) {
                 ++myM;
                 if (rec != nullptr) {
-                  TCHECK(rec_off[d] + rc < rec_off[d + 1], "window record");
+                  TCHECK(rbase + rc < rec_off[d + 1], "window record");
                   Rec r;
                   r.chunk = chunk;
                   r.link = t_lid[q];
                   r.t_start = tk;
-                  rec[rec_off[d] + rc] = r;
+                  rec[rbase + rc] = r;
                 }
               }
               ++rc;
