@@ -14,7 +14,10 @@ python bench.py --config 2 --no-baselines > gpurun_out/bench_c2.json 2>&1
 python bench.py --config 5 --no-baselines > gpurun_out/bench_c5.json 2>&1
 python bench.py --config 4 --steps 5 --warmup 3 --e2e-steps 2 --no-baselines > gpurun_out/bench_c4.json 2>&1
 python bench.py --config 4 --seeds 64 --steps 3 --warmup 3 --e2e-steps 1 --no-baselines --no-cpu-baseline > gpurun_out/bench_c4_s64.json 2>&1
+python bench.py --literal --no-baselines > gpurun_out/bench_c3_literal.json 2>&1
+python bench.py --config 6 --no-baselines > gpurun_out/bench_ctx.json 2>&1
 python tools/host_breakdown.py 3 > gpurun_out/e2e_breakdown_c3.txt 2>&1
+python tools/trace_windows.py 4 > gpurun_out/trace_windows_c4_summary.txt 2>&1
 ARGS="--steps 3 --warmup 3 --no-cpu-baseline --no-baselines --e2e-steps 1"
 python bench.py $ARGS > gpurun_out/plain_small.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py $ARGS > gpurun_out/ncu_launches.log 2>&1
