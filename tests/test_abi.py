@@ -140,3 +140,25 @@ def test_eval_flags_mutations(T):
     s[i]["t_start"] = 0
     s[i]["t_end"] = int(s[i]["t_end"]) - int(base[i]["t_start"])
     assert rep_of(s)["unheld_at_depart"] >= 1
+
+
+def test_multi_device_entry_points_without_gpu(T):
+    """The multi-GPU entry points fail loudly without a device (no CPU fallback), and NCCL is
+    resolved at run time (dlopen): the library reports the version it would use."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    t = T.Topology.from_workload_topology(W.torus([4, 4]))
+    with pytest.raises(T.TacosError) as e:
+        T.synthesize(t, "AR", 1, 1 << 20, 4, n_devices=2)
+    assert e.value.code == T.TACOS_E_CUDA
+    with pytest.raises(T.TacosError) as e:
+        T.synthesize_batch([t, t], collective="AR", n_seeds=2, n_devices=2)
+    assert e.value.code == T.TACOS_E_CUDA
+    try:
+        v = T.nccl_version()
+    except T.TacosError as err:  # no NCCL on this host: the documented error
+        assert err.code == T.TACOS_E_NCCL
+    else:
+        assert v >= 20000
