@@ -1193,74 +1193,101 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 
         // REG_PATH (every in-degree <= kRegDeg): ranks in registers; else shared memory
         if constexpr (REG_PATH && P == 1 && kP1Smem) {
-          // ---- one thread per destination: in-link j in slot j (static), ranks by the
-          //      28 pairwise comparisons, walk order packed 4 bits per rank, and the
-          //      next in-link's source row loaded while the current one is matched ----
-          unsigned long long key[kRegDeg];
-          uint32_t nfree = 0, nlive = 0;
-          // the link state of every slot is loaded before any draw, so the loads of later
-          // slots do not wait behind the Philox chains of earlier ones
-          uint32_t live = 0;  // bit j: slot j is live
-          {
-            unsigned long long bq[kRegDeg];
-            uint32_t sq[kRegDeg], srq[kRegDeg];
+          // ---- one thread per destination: in-link j in slot j (static), ranks by pairwise
+          //      comparisons, walk order packed 4 bits per rank, and the next in-link's source
+          //      row loaded while the current one is matched.  The slot count is specialised:
+          //      D = 6 (15 comparisons, e.g. every 3-D torus) or 8 (28) ----
+          uint32_t nfree = 0, nlive = 0, ordp = 0;  // ordp: slot of rank s in bits [4s, 4s + 4)
+          auto prologue = [&](auto degc) {
+            constexpr int D = decltype(degc)::value;
+            unsigned long long key[D];
+            uint32_t o32[D];
+            // the link state of every slot is loaded before any draw, so the loads of later
+            // slots do not wait behind the Philox chains of earlier ones
+            uint32_t live = 0;  // bit j: slot j is live
+            {
+              unsigned long long bq[D];
+              uint32_t sq[D], srq[D];
 #pragma unroll
-            for (int j = 0; j < kRegDeg; ++j) {
-              const uint32_t q = b0 + (uint32_t)j;
-              const bool in = (uint32_t)j < deg;
-              bq[j] = in ? busy[q] : ~0ull;
-              sq[j] = in ? seen[q] : 0u;
-              srq[j] = in ? (uint32_t)t_src[q] : 0u;
-            }
-#pragma unroll
-            for (int j = 0; j < kRegDeg; ++j) {
-              const bool in = (uint32_t)j < deg;
-              const bool isfree = in && bq[j] <= t;
-              if (in && !isfree) mo_w = (uint32_t)(bq[j] - t) < mo_w ? (uint32_t)(bq[j] - t) : mo_w;
-              nfree += isfree ? 1u : 0u;
-              if (isfree && sq[j] != hver_of(srq[j])) live |= 1u << j;
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) {
-            key[j] = ~0ull;
-            if ((live >> j) & 1u) {
-              const uint32_t q = b0 + (uint32_t)j;
-              uint32_t o;
-              if (pre_draw) {
-                o = ord[q];
-              } else {
-                const uint4 r = philox4x32_10(
-                    make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
-                o = r.x;
-                pick[q] = r.y;
+              for (int j = 0; j < D; ++j) {
+                const uint32_t q = b0 + (uint32_t)j;
+                const bool in = (uint32_t)j < deg;
+                bq[j] = in ? busy[q] : ~0ull;
+                sq[j] = in ? seen[q] : 0u;
+                srq[j] = in ? (uint32_t)t_src[q] : 0u;
               }
-              ++nlive;
-              key[j] = ((unsigned long long)t_w[q] << 32) | o;  // (w, u_ord), R3
+#pragma unroll
+              for (int j = 0; j < D; ++j) {
+                const bool in = (uint32_t)j < deg;
+                const bool isfree = in && bq[j] <= t;
+                if (in && !isfree) mo_w = (uint32_t)(bq[j] - t) < mo_w ? (uint32_t)(bq[j] - t) : mo_w;
+                nfree += isfree ? 1u : 0u;
+                if (isfree && sq[j] != hver_of(srq[j])) live |= 1u << j;
+              }
             }
-          }
+            uint32_t wlo = ~0u, whi = 0u;
+            bool ord_max = false;  // a live u_ord of 2^32 - 1 (then the 32-bit keys could tie a dead slot)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              key[j] = ~0ull;
+              o32[j] = ~0u;
+              if ((live >> j) & 1u) {
+                const uint32_t q = b0 + (uint32_t)j;
+                uint32_t o;
+                if (pre_draw) {
+                  o = ord[q];
+                } else {
+                  const uint4 r = philox4x32_10(
+                      make_uint4((uint32_t)t, (uint32_t)(t >> 32), t_lid[q], job.sigma), seed_lo, seed_hi);
+                  o = r.x;
+                  pick[q] = r.y;
+                }
+                ++nlive;
+                const uint32_t wq = t_w[q];
+                wlo = wq < wlo ? wq : wlo;
+                whi = wq > whi ? wq : whi;
+                ord_max = ord_max || o == ~0u;
+                o32[j] = o;
+                key[j] = ((unsigned long long)wq << 32) | o;  // (w, u_ord), R3
+              }
+            }
+            if (nlive == 0u) return;
+            // rank of slot j = #{i : key_i < key_j or (key_i == key_j and i < j)}; dead keys (~0,
+            // above every live key: w < 2^32 - 1 is enforced on the host) rank last.  With one
+            // cost among the live slots the order is that of u_ord alone (32-bit compares).
+            uint32_t rk[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) rk[j] = 0u;
+            if (wlo == whi && !ord_max) {
+#pragma unroll
+              for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = i + 1; j < D; ++j) {
+                  const bool jfirst = o32[j] < o32[i];
+                  rk[i] += jfirst ? 1u : 0u;
+                  rk[j] += jfirst ? 0u : 1u;
+                }
+            } else {
+#pragma unroll
+              for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = i + 1; j < D; ++j) {
+                  const bool jfirst = key[j] < key[i];
+                  rk[i] += jfirst ? 1u : 0u;
+                  rk[j] += jfirst ? 0u : 1u;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < D; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
+          };
+          if (deg <= 6u) prologue(std::integral_constant<int, 6>());
+          else prologue(std::integral_constant<int, kRegDeg>());
           if (!worklist) {
             myV += nfree;
             myD += nfree ? 1u : 0u;
           }
           if (gl == 0) myL += nlive;
           if (nlive == 0u) continue;
-          // rank of slot j = #{i : key_i < key_j or (key_i == key_j and i < j)}; non-live keys
-          // (~0, above every live key: w < 2^32 - 1 is enforced on the host) rank last
-          uint32_t rk[kRegDeg];
-#pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) rk[j] = 0u;
-#pragma unroll
-          for (int i = 0; i < kRegDeg; ++i)
-#pragma unroll
-            for (int j = i + 1; j < kRegDeg; ++j) {
-              const bool jfirst = key[j] < key[i];
-              rk[i] += jfirst ? 1u : 0u;
-              rk[j] += jfirst ? 0u : 1u;
-            }
-          uint32_t ordp = 0;  // slot of rank s in bits [4s, 4s + 4)
-#pragma unroll
-          for (int j = 0; j < kRegDeg; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
           const long long dbg_pro = job.trace != nullptr ? clock64() : 0;  // debug (TACOS_TRACE)
           uint4 nxt[V];
           if constexpr (!kHaveSmem) {
