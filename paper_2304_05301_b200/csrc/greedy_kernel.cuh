@@ -68,12 +68,19 @@ constexpr bool kP1Smem = true;
 #ifndef TACOS_V4_THREADS  // thread bound of the 4-vector kernels (registers: 65536 / bound per thread)
 #define TACOS_V4_THREADS 384
 #endif
+#ifndef TACOS_WIDE_THREADS  // thread bound of the wide-row kernels (P > 2 lanes, 4 vectors)
+#define TACOS_WIDE_THREADS 512  // 128 registers: 32 lane groups of 16 in flight instead of 24 (config 4: 223 -> 213 ms)
+#endif
+#ifndef TACOS_V2_THREADS  // thread bound of the other 2-vector kernels (tuning; default as the 4-vector ones)
+#define TACOS_V2_THREADS TACOS_V4_THREADS
+#endif
 // thread bound per kernel shape (registers per thread <= 65536 / bound): one vector per lane 768,
 // two-lane groups of two vectors 640 (one group per destination of a 256-destination CTA plus
 // the record warps), otherwise TACOS_V4_THREADS
 template <int P, int V>
 struct ThreadsFor {
-  static constexpr int value = V == 1 ? 768 : (P == 2 && V == 2) ? 640 : TACOS_V4_THREADS;
+  static constexpr int value = V == 1 ? 768 : (P == 2 && V == 2) ? 640 : V == 2 ? TACOS_V2_THREADS
+                                : P > 2 ? TACOS_WIDE_THREADS : TACOS_V4_THREADS;
 };
 // MASKED (relays, R22): candidates are also and-ed with the
 // per-position allow row, and only arrivals of chunks in post[dst] count.

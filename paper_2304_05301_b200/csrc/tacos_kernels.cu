@@ -105,7 +105,9 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   // threads: one destination group per own destination in one pass when possible, plus
   // the warps that write the previous event's records meanwhile (about one thread per 16
   // own in-links; measured on configs 2, 3, 5)
-  const uint32_t th_max = VPL == 1 ? 768u : (P == 2 && VPL == 2) ? 640u : (uint32_t)TACOS_V4_THREADS;  // = ThreadsFor<P, V>
+  const uint32_t th_max = VPL == 1 ? 768u : (P == 2 && VPL == 2) ? 640u
+                          : VPL == 2 ? (uint32_t)TACOS_V2_THREADS
+                          : P > 2u  ? (uint32_t)TACOS_WIDE_THREADS : (uint32_t)TACOS_V4_THREADS;  // = ThreadsFor<P, V>
   const uint32_t walkers = (n_own * P + 31u) & ~31u;
   const uint32_t recw = std::max<uint32_t>(64u, ((L / Q) / 16u + 31u) & ~31u);
   uint32_t th = std::max<uint32_t>(128u, walkers + recw);
