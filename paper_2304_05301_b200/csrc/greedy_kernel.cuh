@@ -97,7 +97,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   __shared__ unsigned long long s_delivered, s_V, s_D, s_M, s_L;
   __shared__ uint32_t s_arr[2], s_min32[2], s_mcnt[2];
   // cluster exchange slots, indexed by the writer's rank (plain remote stores, no 64-bit DSMEM atomics)
-  __shared__ unsigned long long s_slot_deliv[8], s_slot_min[8], s_slot_cnt[8][4];
+  // s_slot_min2: event parity (the lock-step loop has one cluster barrier per event, so a peer may
+  // publish event e + 1 before this CTA has read event e's slots)
+  __shared__ unsigned long long s_slot_deliv[8], s_slot_min2[2][8], s_slot_cnt[8][4];
 
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -165,6 +167,30 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   const bool worklist = lay.worklist != 0u;
   TCHECK(lay.smem_bytes <= dynamic_smem_bytes(), "layout exceeds the dynamic shared memory");
   TCHECK(d_lo <= d_hi && p_lo <= p_hi && p_hi <= L, "CTA ranges");
+  // Lock-step loop (one link cost, one lane per destination, AG-type, no relays; host: add_lockstep):
+  // every send started at t ends at the next event t + w, so the walkers write the arrivals of the
+  // next event themselves into the other held buffer (held[2][N], event parity) and an event needs
+  // one cluster barrier.  Its layout keeps only the CTA's own have rows and in-link positions:
+  // the pointers are shifted so that global indices address them.
+  constexpr bool kLock = REG_PATH && P == 1 && kP1Smem && ROWS_SMEM && LINKS_SMEM && !MASKED;
+  const bool lockstep = kLock && lay.lockstep != 0u;
+  uint32_t *const held_base = held, *const hver_base = hver;
+  if (lockstep) {
+    TCHECK(p_hi - p_lo <= lay.pos_cap, "lock-step position capacity");
+    have = held + (size_t)2u * N * Wr - (size_t)d_lo * Wr;
+    busy -= p_lo;
+    cur -= p_lo;
+    ord -= p_lo;
+    pick -= p_lo;
+    seen -= p_lo;
+    order -= p_lo;
+    rch -= 2u * p_lo;
+    lv -= p_lo;
+    t_src -= p_lo;
+    t_w -= p_lo;
+    t_lid -= p_lo;
+    t_dst -= p_lo;
+  }
   auto cluster_barrier = [&]() {
     if (Q > 1) cluster.sync();
     else __syncthreads();
@@ -219,7 +245,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       const_cast<IdT *>(t_dst)[p] = (IdT)__ldg(&T.p_dst[p]);
     }
   }
-  for (uint32_t x = tid; x < N; x += nthr) hver[x] = 0u;
+  for (uint32_t x = tid; x < (lockstep ? 2u * N : N); x += nthr) hver[x] = 0u;
   for (uint32_t x = d_lo + tid; x < d_hi; x += nthr) s_peers[x] = 0u;
   for (uint32_t x = d_lo + tid; x <= d_hi; x += nthr) s_inptr[x] = __ldg(&in_ptr[x]);
   for (uint32_t i = tid; i < 2u * nbw; i += nthr) bitmap2[i] = 0u;
@@ -810,13 +836,13 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         mo = __reduce_min_sync(0xFFFFFFFFu, mo);
         if (lane == 0 && mo != ~0u) atomicMin(&s_wmin, mo);
         __syncthreads();
-        if (Q > 1 && tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid), (unsigned long long)s_wmin << 32);
+        if (Q > 1 && tid < Q) dsmem_st_u64(dsmem_addr(&s_slot_min2[0][crank], tid), (unsigned long long)s_wmin << 32);
         cluster_barrier();
         uint32_t mo_all = s_wmin;
         if (Q > 1) {
           mo_all = ~0u;
           for (uint32_t r = 0; r < Q; ++r) {
-            const uint32_t hi = (uint32_t)(s_slot_min[r] >> 32);
+            const uint32_t hi = (uint32_t)(s_slot_min2[0][r] >> 32);
             mo_all = hi < mo_all ? hi : mo_all;
           }
         }
@@ -850,6 +876,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
   }
 
+  unsigned long long ls_delivered = 0ull;  // lock-step loop: cluster-wide deliveries up to t
   if (!windowed)
   for (;;) {
     long long ts[9];  // debug phase timestamps (TACOS_TRACE), thread 0
@@ -860,7 +887,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       s_mcnt[e & 1u] = 0u;
     }
     if (worklist && tid == 0) s_nwork = 0u;  // read in PW, after the cluster barrier
-    {
+    if (lockstep) {  // the arrivals at t are in held[e & 1] (written by the walkers of event e - 1)
+      held = held_base + (size_t)(e & 1u) * N * Wr;
+      hver = hver_base + (size_t)(e & 1u) * N;
+    } else {
       uint32_t arr = 0;
       // one thread per in-link position: the arrival (a shared-memory atomicOr on the
       // destination's held row).  With pre_draw the Philox draws of this event were made
@@ -907,10 +937,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       }
     }
     if (tracing) ts[1] = clock64();
-    cluster_barrier();
+    if (!lockstep) cluster_barrier();
     if (tracing) ts[2] = clock64();
-    unsigned long long delivered = s_delivered + s_arr[e & 1u];  // own, cumulative
-    if (Q > 1) {
+    unsigned long long delivered = lockstep ? ls_delivered : s_delivered + s_arr[e & 1u];  // own, cumulative
+    if (Q > 1 && !lockstep) {
       delivered = 0;
       for (uint32_t r = 0; r < Q; ++r) delivered += s_slot_deliv[r];
     }
@@ -1287,6 +1317,29 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int j = 0; j < D; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
           };
+          // lock-step loop: d's held row at the next event = have[d] after the walk (at t every
+          // earlier send has arrived, so have == held; the claims of t arrive at t + w, the next
+          // event), written to the other held buffer and pushed to the CTAs that mirror d
+          auto ls_push = [&](bool arrived) {
+            const uint32_t nb = (e + 1u) & 1u;
+            uint4 *hn = reinterpret_cast<uint4 *>(held_base + ((size_t)nb * N + d) * Wr);
+            uint32_t *hvn = hver_base + (size_t)nb * N + d;
+            uint4 r[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) r[v] = have4[v];
+#pragma unroll
+            for (int v = 0; v < V; ++v) hn[v] = r[v];
+            const uint32_t ver = arrived ? e + 1u : hver[d];
+            *hvn = ver;
+            if (Q > 1)
+              for (uint32_t pm = s_peers[d]; pm; pm &= pm - 1u) {
+                const uint32_t rk = __ffs(pm) - 1u;
+#pragma unroll
+                for (int v = 0; v < V; ++v) dsmem_st_v4(dsmem_addr(hn + v, rk), r[v]);
+                dsmem_st_u32(dsmem_addr(hvn, rk), ver);
+              }
+          };
+          const uint32_t claims0 = my_claims;
           if (deg <= 6u) prologue(std::integral_constant<int, 6>());
           else prologue(std::integral_constant<int, kRegDeg>());
           if (!worklist) {
@@ -1294,7 +1347,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             myD += nfree ? 1u : 0u;
           }
           if (gl == 0) myL += nlive;
-          if (nlive == 0u) continue;
+          if (nlive == 0u) {
+            if (lockstep) ls_push(false);
+            continue;
+          }
           const long long dbg_pro = job.trace != nullptr ? clock64() : 0;  // debug (TACOS_TRACE)
           uint4 nxt[V];
           if constexpr (!kHaveSmem) {
@@ -1325,6 +1381,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) have4[v] = hv[v];
           }
+          if (lockstep) ls_push(my_claims != claims0);
         } else if constexpr (REG_PATH && P <= 2) {
           // ---- a group of P lanes per destination: every lane ranks the in-links itself
           //      (redundant, no shuffles); the row is split lane-major (lane gl holds the
@@ -1748,7 +1805,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       if (lane == 0 && mo != ~0u) atomicMin(&s_min32[e & 1u], mo);
       __syncthreads();
       if (Q > 1 && tid < Q)
-        dsmem_st_u64(dsmem_addr(&s_slot_min[crank], tid),
+        dsmem_st_u64(dsmem_addr(&s_slot_min2[e & 1u][crank], tid),
                      ((unsigned long long)s_min32[e & 1u] << 32) | s_mcnt[e & 1u]);
       if (tracing) ts[6] = clock64();
       if (Q > 1) cluster.sync();
@@ -1759,7 +1816,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       mo_all = ~0u;
       m_all = 0u;
       for (uint32_t r = 0; r < Q; ++r) {
-        const unsigned long long v = s_slot_min[r];
+        const unsigned long long v = s_slot_min2[e & 1u][r];
         const uint32_t hi = (uint32_t)(v >> 32);
         mo_all = hi < mo_all ? hi : mo_all;
         m_all += (uint32_t)v;
@@ -1768,6 +1825,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     const unsigned long long tn = mo_all == ~0u ? ~0ull : t + mo_all;
     rb_prev = rb;
     rb += m_all;
+    if (lockstep) ls_delivered += m_all;  // AG without relays: every send is a delivery at t + w
     if (pre_draw && tn != ~0ull) draw_ahead(tn, tid, nthr);  // (optional) the next event's draws
     if (tracing && e % job.trace_stride == 0u && e / job.trace_stride < kTraceEvents) {
       ts[8] = clock64();

@@ -900,6 +900,26 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         add_window(l2, maxN, 0, 0);
         lq = l2;
       }
+      // Lock-step loop (greedy_kernel.cuh): one link cost per topology, one lane per
+      // destination on the register path, AG-type problem without relays: every send started at t
+      // ends at the next event t + w, so the walkers write the arrivals themselves (held rows
+      // double-buffered by event parity) and an event needs one cluster barrier.  TACOS_LOCKSTEP=0: off.
+      const char *env_ls = getenv("TACOS_LOCKSTEP");
+      if (!win && !multi_w && P0 == 1u && lq.reg_path && !relay && !custom && !(p->flags & TACOS_FLAG_LITERAL) &&
+          !lq.worklist && (!env_ls || atoi(env_ls) != 0)) {
+        const uint32_t Q = lq.cluster;
+        uint32_t pos_cap = 0;
+        for (size_t gk = gi; gk < gj; ++gk) {
+          const tacos_topology *tt = pl->parts[order[gk]].topo;
+          const uint32_t n = (uint32_t)tt->N, chunk_n = (n + Q - 1u) / Q;
+          for (int o = 0; o < 2; ++o)
+            for (uint32_t r = 0; r < Q; ++r) {
+              const uint32_t lo = std::min(n, r * chunk_n), hi = std::min(n, lo + chunk_n);
+              pos_cap = std::max(pos_cap, tt->in_ptr[o][hi] - tt->in_ptr[o][lo]);
+            }
+        }
+        add_lockstep(lq, maxN, std::max(pos_cap, 1u), smem_limit);
+      }
     };
     finish_layout(g.lay);
     // Cluster size: the largest Q <= 8 (any size, not only powers of two) with jobs * Q <= #SMs,

@@ -89,11 +89,18 @@ struct Layout {
   // iteration), max in-degree, and its shared-memory arrays (after the others)
   uint32_t window, win_deg, win_ev;  // win_ev: events per window at most (<= kWinEv; TACOS_WIN_EV)
   uint32_t off_wbm, off_wev, off_wevc, off_wevo, off_wacnt, off_waoff, off_wachk;
+  // lock-step event loop (one link cost, one lane per destination): held rows
+  // double-buffered by event parity (held[2][N], then the own have rows), link state of the
+  // CTA's own in-link positions only (pos_cap per CTA), hver[2][N]
+  uint32_t lockstep, pos_cap;
 };
 constexpr uint32_t kWinEv = 256;      // events per window at most (a longer window is cut there)
 constexpr uint32_t kWinBits = 16384;  // window length cap (bitmap of event offsets)
 // Append the windowed loop's shared-memory arrays to a layout (window = W, deg = max in-degree).
 void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg);
+// Switch a one-lane shared-memory layout to the lock-step loop's (pos_cap = the most in-link
+// positions a CTA of the cluster owns); false (layout unchanged) when it does not fit.
+bool add_lockstep(Layout &lay, uint32_t N, uint32_t pos_cap, size_t smem_limit);
 
 // q_force: cluster size to use (0: the automatic choice; TACOS_CLUSTER overrides both)
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,

@@ -144,6 +144,45 @@ void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg) {
   lay.smem_bytes = s;
 }
 
+bool add_lockstep(Layout &lay, uint32_t N, uint32_t pos_cap, size_t smem_limit) {
+  auto al = [](uint32_t x, uint32_t a) { return (x + a - 1u) / a * a; };
+  if (!lay.rows_in_smem || !lay.links_in_smem || lay.window || lay.pre_draw) return false;
+  Layout l = lay;
+  const uint32_t Q = l.cluster, n_own = (N + Q - 1u) / Q, Lc = pos_cap;
+  l.rows_bytes = al((2u * N + n_own) * l.row_stride * 4u, 16u);  // held[2][N], have[n_own]
+  uint32_t o = 0;
+  l.off_busy = o; o += al(Lc * 8u, 16u);
+  l.off_cur = o; o += al(Lc * 4u, 16u);
+  l.off_ord = o; o += al(Lc * 4u, 16u);
+  l.off_pick = o; o += al(Lc * 4u, 16u);
+  l.off_seen = o; o += al(Lc * 4u, 16u);
+  l.off_order = o; o += al(Lc * 2u, 16u);
+  l.off_rch = o; o += al(Lc * 4u, 16u);
+  l.off_tsrc = o; o += al(Lc * 2u, 16u);
+  l.off_tw = o; o += al(Lc * 4u, 16u);
+  l.off_tlid = o; o += al(Lc * 2u, 16u);
+  l.off_tdst = o; o += al(Lc * 2u, 16u);
+  l.off_lv = o; o += al(Lc, 16u);
+  l.links_bytes = o;
+  // the small arrays keep their sizes (hver doubles); shift them behind the new regions
+  const uint32_t old_base = lay.off_hver, new_base = l.rows_bytes + l.links_bytes;
+  const uint32_t hv_old = al(N * 4u, 16u), hv_new = al(2u * N * 4u, 16u);
+  auto mv = [&](uint32_t off) { return off - old_base - hv_old + new_base + hv_new; };
+  l.off_hver = new_base;
+  l.off_bitmap = mv(lay.off_bitmap);
+  l.off_wpre = mv(lay.off_wpre);
+  l.off_inptr = mv(lay.off_inptr);
+  l.off_act = mv(lay.off_act);
+  l.off_list = mv(lay.off_list);
+  l.off_peers = mv(lay.off_peers);
+  l.smem_bytes = mv(lay.smem_bytes);
+  if ((size_t)l.smem_bytes > smem_limit) return false;
+  l.lockstep = 1u;
+  l.pos_cap = pos_cap;
+  lay = l;
+  return true;
+}
+
 int launch_greedy(const Layout &lay, uint32_t P, uint32_t VPL, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs,
                   void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
