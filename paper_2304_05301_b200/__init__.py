@@ -94,7 +94,8 @@ class tacos_winner(ctypes.Structure):
 class tacos_plan_info(ctypes.Structure):
     _fields_ = [("n_jobs", ctypes.c_uint32), ("ctas", ctypes.c_uint32), ("cluster", ctypes.c_uint32),
                 ("threads", ctypes.c_uint32), ("smem_bytes", ctypes.c_uint32), ("rows_in_smem", ctypes.c_uint32),
-                ("links_in_smem", ctypes.c_uint32), ("launches", ctypes.c_uint32), ("rows_bytes", ctypes.c_uint64)]
+                ("links_in_smem", ctypes.c_uint32), ("launches", ctypes.c_uint32), ("rows_bytes", ctypes.c_uint64),
+                ("event_loop", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class tacos_cont_report(ctypes.Structure):

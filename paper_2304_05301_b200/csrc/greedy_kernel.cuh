@@ -287,25 +287,28 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     };
     const uint32_t par = (ev + 1u) & 1u;
     uint32_t *bmp = bitmap2 + par * nbw;
+    // bitmap keys: link ids (cluster-wide bitmap), or in the lock-step loop the CTA's own
+    // positions q - p_lo (its records follow those of the lower cluster ranks: base)
+    const uint32_t nkw = lockstep ? (p_hi - p_lo + 31u) / 32u : nbw;
     if (tid - first < 32u) {
       uint32_t running = 0;
-      for (uint32_t b = 0; b < nbw; b += 32u) {
+      for (uint32_t b = 0; b < nkw; b += 32u) {
         const uint32_t i = b + lane;
-        const uint32_t v = i < nbw ? __popc(bmp[i]) : 0u;
+        const uint32_t v = i < nkw ? __popc(bmp[i]) : 0u;
         uint32_t incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
           if (lane >= (uint32_t)o) incl += y;
         }
-        if (i < nbw) wpre[i] = running + incl - v;
+        if (i < nkw) wpre[i] = running + incl - v;
         running += __shfl_sync(0xFFFFFFFFu, incl, 31);
       }
     }
     group_sync();
     for (uint32_t q = p_lo + (tid - first); q < p_hi; q += count) {
-      const uint32_t lid = t_lid[q];
-      const uint32_t wi = lid >> 5, word = bmp[wi], bit = 1u << (lid & 31u);
+      const uint32_t lid = t_lid[q], key = lockstep ? q - p_lo : lid;
+      const uint32_t wi = key >> 5, word = bmp[wi], bit = 1u << (key & 31u);
       if (word & bit) {
         Rec rc;
         rc.chunk = rch[2u * q + par];
@@ -317,7 +320,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     }
     if (clear) {
       group_sync();
-      for (uint32_t i = tid - first; i < nbw; i += count) bmp[i] = 0u;
+      for (uint32_t i = tid - first; i < nkw; i += count) bmp[i] = 0u;
     }
   };
   uint32_t rb = 0, rb_prev = 0;  // record offsets of the matches of events e and e-1 (cluster-wide)
@@ -1037,6 +1040,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         TCHECK(d >= d_lo && d < d_hi && b0 >= p_lo && b1 <= p_hi && b0 <= b1, "destination range");
         uint4 *have4 = reinterpret_cast<uint4 *>(have + (size_t)d * Wr);
         uint4 hv[V];
+        uint32_t pmask = 0;  // lock-step loop: matched in-link slots of d (bit p - b0)
 
         // One step of the matching walk (a5) on in-link position p with pick draw pk.
         // held[src] row of in-link p into registers (own shared memory, a peer's via DSMEM, or L2)
@@ -1122,15 +1126,19 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
           const uint32_t chunk = (vsel * 4u + wi) * 32u + bit;
           TCHECK(chunk < T.C && t_lid[p] < L, "claimed chunk");
-          cur[p] = chunk;
+          if (!lockstep) cur[p] = chunk;  // (the lock-step loop has no arrival phase)
           rch[2u * p + (e & 1u)] = (uint16_t)chunk;
           const uint32_t wp = t_w[p];
           busy[p] = t + wp;
           mo_w = wp < mo_w ? wp : mo_w;
           ++myM;
           ++my_claims;
-          const uint32_t lid = t_lid[p];
-          atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
+          if (lockstep) {  // position bits, set once per destination after the walk
+            pmask |= 1u << (p - b0);
+          } else {
+            const uint32_t lid = t_lid[p];
+            atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
+          }
         };
 
         // One step of the matching walk (a5) on in-link p, pick draw pk, loaded row cv.
@@ -1381,7 +1389,14 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) have4[v] = hv[v];
           }
-          if (lockstep) ls_push(my_claims != claims0);
+          if (lockstep) {
+            ls_push(my_claims != claims0);
+            // this event's matched positions (bit q - p_lo of the CTA's position bitmap): the
+            // records are written in position order, ranked by link at emission
+            const uint32_t o = b0 - p_lo, sh = o & 31u;
+            if (pmask) atomicOr(&bm[o >> 5], pmask << sh);
+            if (sh != 0u && (pmask >> (32u - sh)) != 0u) atomicOr(&bm[(o >> 5) + 1u], pmask >> (32u - sh));
+          }
         } else if constexpr (REG_PATH && P <= 2) {
           // ---- a group of P lanes per destination: every lane ranks the in-links itself
           //      (redundant, no shuffles); the row is split lane-major (lane gl holds the
@@ -1784,7 +1799,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       uint32_t *bm = bitmap2 + (e & 1u) * nbw;
       // publish: own matched links into the peers' bitmaps; own min busy_until (as an offset
       // from t, < 2^32) and own match count into every CTA's slot
-      if (Q > 1) {
+      if (Q > 1 && !lockstep) {
         for (uint32_t i = tid; i < nbw; i += nthr) {
           const uint32_t wbits = bm[i];
           if (wbits)
@@ -1811,7 +1826,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       if (Q > 1) cluster.sync();
       if (tracing) ts[7] = clock64();
     }
-    uint32_t mo_all = s_min32[e & 1u], m_all = s_mcnt[e & 1u];
+    uint32_t mo_all = s_min32[e & 1u], m_all = s_mcnt[e & 1u], m_lower = 0u;
     if (Q > 1) {
       mo_all = ~0u;
       m_all = 0u;
@@ -1820,10 +1835,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         const uint32_t hi = (uint32_t)(v >> 32);
         mo_all = hi < mo_all ? hi : mo_all;
         m_all += (uint32_t)v;
+        if (r < crank) m_lower += (uint32_t)v;  // matches of the lower cluster ranks at this event
       }
     }
     const unsigned long long tn = mo_all == ~0u ? ~0ull : t + mo_all;
-    rb_prev = rb;
+    rb_prev = lockstep ? rb + m_lower : rb;  // lock-step: this CTA's first record of the event
     rb += m_all;
     if (lockstep) ls_delivered += m_all;  // AG without relays: every send is a delivery at t + w
     if (pre_draw && tn != ~0ull) draw_ahead(tn, tid, nthr);  // (optional) the next event's draws

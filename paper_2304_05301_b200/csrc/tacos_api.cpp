@@ -471,6 +471,7 @@ struct Part {
   bool custom = false, symmetric = false, rs_search = false;
   uint32_t rs_base = 0;  // first job of the G^T (sigma 1) search: S, or 0 when only the RS phase is searched
   bool windowed = false;  // searched by the windowed event loop (records per destination, sorted at emission)
+  bool lockstep = false;  // lock-step loop: records in (t_start, CTA, position) order, ranked by link at emission
   uint64_t required = 0;
   uint64_t cap = 0;  // send records per job (= required without relays)
   std::vector<uint32_t> w;
@@ -959,7 +960,10 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
                   smem_limit);
     g.job_begin = begin;
     g.job_end = n_jobs;
-    for (size_t gk = gi; gk < gj; ++gk) pl->parts[order[gk]].windowed = g.lay.window != 0u;
+    for (size_t gk = gi; gk < gj; ++gk) {
+      pl->parts[order[gk]].windowed = g.lay.window != 0u;
+      pl->parts[order[gk]].lockstep = g.lay.lockstep != 0u;
+    }
     pl->groups.push_back(g);
     gi = gj;
   }
@@ -988,7 +992,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       if ((rc = dev_alloc(bufs, dev, sizeof(Rec) * pt.cap * pt.n_jobs, &vp))) return rc;
       pt.d_rec = reinterpret_cast<Rec *>(vp);
     }
-    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL) || pt.windowed) && record) max_M = std::max(max_M, pt.cap);
+    if ((need_rs || (p->flags & TACOS_FLAG_LITERAL) || pt.windowed || pt.lockstep) && record) max_M = std::max(max_M, pt.cap);
   }
   if (max_M) {
     pl->sort_bytes = rs_sort_scratch_bytes(max_M);
@@ -1242,6 +1246,7 @@ bool dev_emit_eligible(const tacos_plan *pl) {
   const Part &pt = pl->parts[0];
   if (pl->p.flags & (TACOS_FLAG_NO_SCHEDULE | TACOS_FLAG_LITERAL)) return false;
   if (coll_relay(&pl->p) || pt.windowed || pt.d_rec == nullptr) return false;
+  if (pt.lockstep && (size_t)8 * ((pt.L + 31u) / 32u) > (size_t)200 * 1024) return false;
   if (coll_need_rs(pl->p.collective)) {
     if (!pt.symmetric || pt.w.empty() || (size_t)8 * ((pt.L + 31u) / 32u) > (size_t)200 * 1024) return false;
     for (uint32_t x : pt.w)
@@ -1268,9 +1273,17 @@ int plan_emit_dev_launch(tacos_plan *pl, tacos_send *d_sends, uint64_t capacity,
   }
   if (coll_need_ag(coll)) {
     const uint64_t base = coll == TACOS_ALL_REDUCE ? M : 0;
-    if ((rc = launch_emit_ag(nullptr, M, pt.td->d_src, pt.td->d_dst, pt.d_w, 0, d_sends + base, st, ~0ull, &dw)))
-      return fail(rc, "%s", cuda_error_string());
-    pl->last_launches += 1;
+    if (pt.lockstep) {  // records in (t_start, CTA, position) order: ranked by link inside each event
+      uint32_t nl = 0;
+      if ((rc = launch_rs_uniform_emit(nullptr, M, pt.td->d_src, pt.td->d_dst, pt.w[0], nullptr, 0, pt.L, d_sends + base,
+                                       pl->d_sort, pl->sort_bytes, &nl, st, &dw, /*mirror=*/0u)))
+        return fail(rc, "%s", cuda_error_string());
+      pl->last_launches += nl;
+    } else {
+      if ((rc = launch_emit_ag(nullptr, M, pt.td->d_src, pt.td->d_dst, pt.d_w, 0, d_sends + base, st, ~0ull, &dw)))
+        return fail(rc, "%s", cuda_error_string());
+      pl->last_launches += 1;
+    }
   }
   return TACOS_OK;
 }
@@ -1376,6 +1389,19 @@ int plan_emit_part(tacos_plan *pl, size_t i, tacos_send *d_sends, uint64_t capac
     const Rec *rec = pt.d_rec + (size_t)(g_ag - off) * pt.cap;
     const uint64_t base = coll == TACOS_ALL_REDUCE ? pt.required : 0;  // AR: after the RS half (no relays)
     if ((pl->p.flags & TACOS_FLAG_LITERAL) || pt.windowed) {  // records not in (t_start, link) order: sort
+      uint32_t nl = 0;
+      if ((rc = launch_rs_sort_emit(rec, M, pt.td->d_src, pt.td->d_dst, pt.d_w, nullptr, T_ag, pt.L, d_sends + base, pl->d_sort,
+                                    pl->sort_bytes, &nl, st, /*mirror=*/0u, /*shift=*/T_rs)))
+        return fail(rc, "%s", cuda_error_string());
+      pl->last_launches += nl;
+    } else if (pt.lockstep && (size_t)8 * ((pt.L + 31u) / 32u) <= (size_t)200 * 1024) {
+      // records in (t_start, CTA, position) order: ranked by link inside each event (no relays)
+      uint32_t nl = 0;
+      if ((rc = launch_rs_uniform_emit(rec, M, pt.td->d_src, pt.td->d_dst, pt.w[0], nullptr, T_rs, pt.L, d_sends + base,
+                                       pl->d_sort, pl->sort_bytes, &nl, st, nullptr, /*mirror=*/0u)))
+        return fail(rc, "%s", cuda_error_string());
+      pl->last_launches += nl;
+    } else if (pt.lockstep) {  // (a link-id bitmap beyond 200 KB) sort
       uint32_t nl = 0;
       if ((rc = launch_rs_sort_emit(rec, M, pt.td->d_src, pt.td->d_dst, pt.d_w, nullptr, T_ag, pt.L, d_sends + base, pl->d_sort,
                                     pl->sort_bytes, &nl, st, /*mirror=*/0u, /*shift=*/T_rs)))
@@ -1519,6 +1545,7 @@ extern "C" int tacos_plan_info_get(const tacos_plan *pl, tacos_plan_info *out) {
     out->smem_bytes = big->lay.smem_bytes;
     out->rows_in_smem = big->lay.rows_in_smem;
     out->links_in_smem = big->lay.links_in_smem;
+    out->event_loop = big->lay.window ? 1u : big->lay.lockstep ? 2u : 0u;
   }
   return TACOS_OK;
 }

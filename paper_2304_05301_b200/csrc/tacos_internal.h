@@ -132,7 +132,8 @@ int launch_rs_sort_emit(const Rec *rec, uint64_t M, const uint32_t *src, const u
                         uint64_t shift = 0);
 int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, uint32_t w0,
                            const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
-                           size_t scratch_bytes, uint32_t *launches, void *stream, const DevWin *dw = nullptr);
+                           size_t scratch_bytes, uint32_t *launches, void *stream, const DevWin *dw = nullptr,
+                           uint32_t mirror = 1);
 int launch_literal(const Layout &lay, uint32_t VPL, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, void *stream);
 size_t rs_sort_scratch_bytes(uint64_t M);
 int launch_philox_probe(const uint32_t *d_in, uint32_t *d_out, void *stream);

@@ -612,15 +612,20 @@ __global__ void seg_starts_kernel(const Rec *__restrict__ rec, uint64_t M, uint3
   }
 }
 
+// mirror = 0 (AG records of the lock-step loop, in (t_start, CTA, position) order): the same
+// segment ranking with the identity link map puts record i at (start of its segment) + the rank
+// of link_i among the segment's links, i.e. in (t_start, link) order, times shifted by T_rs.
 __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, const uint32_t *__restrict__ starts,
                                        const unsigned int *__restrict__ n_seg, const unsigned char *__restrict__ flags,
                                        uint64_t n_flags, const uint32_t *__restrict__ src,
                                        const uint32_t *__restrict__ dst, uint32_t w0, const int32_t *__restrict__ rev,
-                                       uint64_t T_rs, uint32_t L, Send32 *__restrict__ out, DevWin dw) {
+                                       uint64_t T_rs, uint32_t L, Send32 *__restrict__ out, DevWin dw, uint32_t mirror) {
   extern __shared__ uint32_t sm[];
   if (dw.keys) {
-    rec = dev_winner(dw, T_rs);
+    uint64_t T;
+    rec = dev_winner(dw, T);
     if (!rec) return;
+    T_rs = mirror ? T : (dw.shift_by_T ? T : 0ull);
   }
   const uint32_t nbw = (L + 31u) / 32u;
   uint32_t *bm = sm, *pre = sm + nbw;
@@ -657,7 +662,7 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
     }
     const uint64_t e = s_end;
     for (uint64_t i = s + tid; i < e; i += blockDim.x) {
-      const uint32_t l2 = (uint32_t)rev[rec[i].link];
+      const uint32_t l2 = mirror ? (uint32_t)rev[rec[i].link] : rec[i].link;
       atomicOr(&bm[l2 >> 5], 1u << (l2 & 31u));
     }
     __syncthreads();
@@ -677,18 +682,18 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
       }
     }
     __syncthreads();
-    const uint64_t base = M - e;
+    const uint64_t base = mirror ? M - e : s;
     for (uint64_t i = s + tid; i < e; i += blockDim.x) {
       const Rec r = rec[i];
-      const uint32_t l2 = (uint32_t)rev[r.link];
+      const uint32_t l2 = mirror ? (uint32_t)rev[r.link] : r.link;
       const uint32_t rank = pre[l2 >> 5] + __popc(bm[l2 >> 5] & ((1u << (l2 & 31u)) - 1u));
       Send32 o;
       o.chunk = r.chunk;
       o.link = l2;
       o.src = src[l2];
       o.dst = dst[l2];
-      o.t0 = T_rs - (r.t_start + w0);
-      o.t1 = T_rs - r.t_start;
+      o.t0 = mirror ? T_rs - (r.t_start + w0) : r.t_start + T_rs;
+      o.t1 = mirror ? T_rs - r.t_start : r.t_start + w0 + T_rs;
       out[base + rank] = o;
     }
     __syncthreads();
@@ -697,7 +702,7 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
 
 int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, const uint32_t *dst, uint32_t w0,
                            const int32_t *rev, uint64_t T_rs, uint32_t L, void *out_sends, void *scratch,
-                           size_t scratch_bytes, uint32_t *launches, void *stream, const DevWin *dw) {
+                           size_t scratch_bytes, uint32_t *launches, void *stream, const DevWin *dw, uint32_t mirror) {
   const DevWin dwv = dw ? *dw : DevWin{};
   cudaStream_t st = (cudaStream_t)stream;
   if (M == 0) return 0;
@@ -724,7 +729,7 @@ int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, cons
     }
   }
   rs_uniform_emit_kernel<<<148, 1024, smem, st>>>(rec, M, starts, n_seg, flags, n_flags, src, dst, w0, rev, T_rs, L,
-                                                   reinterpret_cast<Send32 *>(out_sends), dwv);
+                                                   reinterpret_cast<Send32 *>(out_sends), dwv, mirror);
   if (launches) *launches += 2;
   return check_launch("rs_uniform_emit_kernel");
 }

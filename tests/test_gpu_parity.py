@@ -504,3 +504,47 @@ def test_plan_emit_async_device_winner(T):
     buf = torch.empty(pw.n_sends * 32, dtype=torch.uint8, device="cuda")
     assert not pw.emit_async(buf.data_ptr(), pw.n_sends, st)
     assert pw.emit(buf.data_ptr(), pw.n_sends, st)["n_sends"] == pw.n_sends
+
+
+# --------------------------------------------------------------------------
+# the lock-step event loop (one link cost, one lane per destination, AG-type, no relays):
+# walkers write the next event's arrivals into the other held buffer, one cluster barrier per
+# event, records in (t_start, CTA, position) order ranked by link at emission
+# --------------------------------------------------------------------------
+def _lockstep_case(name):
+    return {
+        "torus8x8x8_k1_ar": (W.torus([8, 8, 8]), 1, "AR", 6),
+        "torus4x4_k2_ar": (W.torus([4, 4]), 2, "AR", 7),
+        "torus8x8_k4_ag": (W.torus([8, 8]), 4, "AG", 5),
+        "torus8x8_k4_rs": (W.torus([8, 8]), 4, "RS", 5),
+        "uni_ring9_ar": (W.uni_ring(9), 3, "AR", 4),  # asymmetric: RS searched on G^T (sigma 1 jobs)
+        "hypercube6_k2_ar": (W.hypercube(6), 2, "AR", 4),
+        "mesh6x5_uniform_ar": (W.mesh2d(6, 5, 100, 100), 2, "AR", 4),  # border NPUs: in-degree 2 to 4
+    }[name]
+
+
+@pytest.mark.parametrize("q", ["", "1", "2", "3", "8"])
+@pytest.mark.parametrize("name", ["torus8x8x8_k1_ar", "torus4x4_k2_ar", "torus8x8_k4_ag", "torus8x8_k4_rs",
+                                  "uni_ring9_ar", "hypercube6_k2_ar", "mesh6x5_uniform_ar"])
+def test_lockstep_loop_parity(T, monkeypatch, name, q):
+    topo, k, coll, seeds = _lockstep_case(name)
+    if q:
+        monkeypatch.setenv("TACOS_CLUSTER", q)
+    syn, sch, t = run_both(T, topo, k, 1 << 20, coll, seeds)
+    assert_parity(syn, sch, coll)
+    # (one CTA cannot hold the 512-NPU torus's double-buffered rows: the per-event loop then)
+    fits = not (name == "torus8x8x8_k1_ar" and q == "1")
+    assert T.Plan(t, coll, k, 1 << 20, seeds).info()["event_loop"] == (2 if fits else 0)
+
+
+@pytest.mark.parametrize("name", ["torus8x8x8_k1_ar", "uni_ring9_ar", "torus8x8_k4_ag"])
+def test_lockstep_equals_per_event_loop(T, monkeypatch, name):
+    """Same schedules, times and counters with the lock-step loop off (TACOS_LOCKSTEP=0)."""
+    topo, k, coll, seeds = _lockstep_case(name)
+    t = T.Topology.from_workload_topology(topo)
+    a = T.synthesize(t, coll, k, 1 << 20, seeds, keep_seed_times=True)
+    monkeypatch.setenv("TACOS_LOCKSTEP", "0")
+    assert T.Plan(t, coll, k, 1 << 20, seeds).info()["event_loop"] == 0
+    b = T.synthesize(t, coll, k, 1 << 20, seeds, keep_seed_times=True)
+    assert a.sends.tobytes() == b.sends.tobytes() and a.result == b.result
+    assert np.array_equal(a.seed_times, b.seed_times)
