@@ -1786,6 +1786,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
     if (pm_thr == nthr) write_records(0u, nthr, e, rb_prev, t_prev, true);
     my_claims = __reduce_add_sync(0xFFFFFFFFu, my_claims);
     if (lane == 0 && my_claims) atomicAdd(&s_mcnt[e & 1u], my_claims);
+    // lock-step loop: the walkers' minimum next-free offset joins the same block barrier
+    if (lockstep) {
+      const uint32_t mo = __reduce_min_sync(0xFFFFFFFFu, mo_w);
+      if (lane == 0 && mo != ~0u) atomicMin(&s_min32[e & 1u], mo);
+    }
     if (tracing) ts[4] = clock64();
     __syncthreads();
     if (tracing) ts[5] = clock64();
@@ -1816,9 +1821,11 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           const uint32_t o = (uint32_t)(busy[p] - t);
           mo = o < mo ? o : mo;
         }
-      mo = __reduce_min_sync(0xFFFFFFFFu, mo);
-      if (lane == 0 && mo != ~0u) atomicMin(&s_min32[e & 1u], mo);
-      __syncthreads();
+      if (!lockstep) {
+        mo = __reduce_min_sync(0xFFFFFFFFu, mo);
+        if (lane == 0 && mo != ~0u) atomicMin(&s_min32[e & 1u], mo);
+        __syncthreads();
+      }
       if (Q > 1 && tid < Q)
         dsmem_st_u64(dsmem_addr(&s_slot_min2[e & 1u][crank], tid),
                      ((unsigned long long)s_min32[e & 1u] << 32) | s_mcnt[e & 1u]);
