@@ -99,7 +99,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   // cluster exchange slots, indexed by the writer's rank (plain remote stores, no 64-bit DSMEM atomics)
   // s_slot_min2: event parity (the lock-step loop has one cluster barrier per event, so a peer may
   // publish event e + 1 before this CTA has read event e's slots)
-  __shared__ unsigned long long s_slot_deliv[8], s_slot_min2[2][8], s_slot_cnt[8][4];
+  __shared__ unsigned long long s_slot_deliv[kMaxCluster], s_slot_min2[2][kMaxCluster], s_slot_cnt[kMaxCluster][4];
 
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -1927,6 +1927,8 @@ template <int P, int V, bool R, bool K, bool G, bool M = false>
 int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
   auto fn = greedy_kernel<P, V, R, K, G, M>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.smem_bytes);
+  // clusters beyond the portable 8 CTAs (B200: up to 16) are opt-in per kernel
+  if (e == cudaSuccess && lay.cluster > 8u) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   // all of the unified L1 / shared array as shared memory (the kernels stage their state there;
   // global row loads bypass L1 with ld.cg), so several CTAs can be resident when they fit
   if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

@@ -940,7 +940,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
       }
     } else if (!(p->flags & TACOS_FLAG_LITERAL) && !getenv("TACOS_CLUSTER")) {
       const uint32_t jobs = n_jobs - begin;
-      for (uint32_t q = 8; q > g.lay.cluster; --q) {
+      for (uint32_t q = kMaxCluster; q > g.lay.cluster; --q) {
         if ((uint64_t)jobs * q > (uint64_t)n_sms || maxN / q < 64u) continue;
         Layout lq = make_layout(maxN, maxL, maxW, P0, V0, smem_limit, jobs, (uint32_t)n_sms, q);
         finish_layout(lq);
@@ -1246,7 +1246,7 @@ bool dev_emit_eligible(const tacos_plan *pl) {
   const Part &pt = pl->parts[0];
   if (pl->p.flags & (TACOS_FLAG_NO_SCHEDULE | TACOS_FLAG_LITERAL)) return false;
   if (coll_relay(&pl->p) || pt.windowed || pt.d_rec == nullptr) return false;
-  if (pt.lockstep && (size_t)8 * ((pt.L + 31u) / 32u) > (size_t)200 * 1024) return false;
+  if (pt.lockstep && (size_t)16 * ((pt.L + 31u) / 32u) > (size_t)200 * 1024) return false;
   if (coll_need_rs(pl->p.collective)) {
     if (!pt.symmetric || pt.w.empty() || (size_t)8 * ((pt.L + 31u) / 32u) > (size_t)200 * 1024) return false;
     for (uint32_t x : pt.w)
@@ -1264,6 +1264,14 @@ int plan_emit_dev_launch(tacos_plan *pl, tacos_send *d_sends, uint64_t capacity,
             pl->p.n_seeds, coll == TACOS_ALL_REDUCE ? 1u : 0u};
   const uint64_t M = pt.required;
   int rc;
+  if (coll == TACOS_ALL_REDUCE && pt.lockstep) {  // both phases from one pass over the records
+    uint32_t nl = 0;
+    if ((rc = launch_rs_uniform_emit(nullptr, M, pt.td->d_src, pt.td->d_dst, pt.w[0], pt.td->d_rev, 0, pt.L, d_sends,
+                                     pl->d_sort, pl->sort_bytes, &nl, st, &dw, /*mirror=*/2u)))
+      return fail(rc, "%s", cuda_error_string());
+    pl->last_launches += nl;
+    return TACOS_OK;
+  }
   if (coll_need_rs(coll)) {
     uint32_t nl = 0;
     if ((rc = launch_rs_uniform_emit(nullptr, M, pt.td->d_src, pt.td->d_dst, pt.w[0], pt.td->d_rev, 0, pt.L, d_sends,

@@ -94,6 +94,7 @@ struct Layout {
   // CTA's own in-link positions only (pos_cap per CTA), hver[2][N]
   uint32_t lockstep, pos_cap;
 };
+constexpr uint32_t kMaxCluster = 16;  // CTAs per job at most (non-portable cluster sizes above 8)
 constexpr uint32_t kWinEv = 256;      // events per window at most (a longer window is cut there)
 constexpr uint32_t kWinBits = 16384;  // window length cap (bitmap of event offsets)
 // Append the windowed loop's shared-memory arrays to a layout (window = W, deg = max in-degree).

@@ -98,7 +98,7 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   if (q_force) Q = q_force;
   if (const char *env = getenv("TACOS_CLUSTER")) {
     const uint32_t want = (uint32_t)atoi(env);
-    if (want >= 1 && want <= 8) Q = want;  // any cluster size up to the portable 8
+    if (want >= 1 && want <= kMaxCluster) Q = want;  // any cluster size (above 8: non-portable)
   }
   lay.cluster = Q;
   const uint32_t n_own = (N + Q - 1) / Q;
@@ -615,6 +615,8 @@ __global__ void seg_starts_kernel(const Rec *__restrict__ rec, uint64_t M, uint3
 // mirror = 0 (AG records of the lock-step loop, in (t_start, CTA, position) order): the same
 // segment ranking with the identity link map puts record i at (start of its segment) + the rank
 // of link_i among the segment's links, i.e. in (t_start, link) order, times shifted by T_rs.
+// mirror = 2: both phases of an AR from one read of the records (RS at out[0, M), AG at
+// out[M, 2M) shifted by T_rs = T_AG; a symmetric AR's two phases come from the same seed).
 __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, const uint32_t *__restrict__ starts,
                                        const unsigned int *__restrict__ n_seg, const unsigned char *__restrict__ flags,
                                        uint64_t n_flags, const uint32_t *__restrict__ src,
@@ -628,13 +630,16 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
     T_rs = mirror ? T : (dw.shift_by_T ? T : 0ull);
   }
   const uint32_t nbw = (L + 31u) / 32u;
-  uint32_t *bm = sm, *pre = sm + nbw;
+  const bool doR = mirror != 0u, doA = mirror != 1u;
+  // side 0: reverse links (RS), side 1: link ids (AG); a bitmap and its prefix each
+  uint32_t *bmR = sm, *preR = sm + nbw;
+  uint32_t *bmA = doR ? sm + 2u * nbw : sm, *preA = bmA + nbw;
   __shared__ unsigned long long s_end;
-  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const unsigned int nseg = *n_seg;
   for (uint32_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
     const uint64_t s = starts[sg];
-    for (uint32_t i = tid; i < nbw; i += blockDim.x) bm[i] = 0u;
+    for (uint32_t i = tid; i < (doR && doA ? 2u : 1u) * 2u * nbw; i += blockDim.x) sm[i] = 0u;
     if (tid == 0) s_end = M;
     __syncthreads();
     // segment end: the next segment start after s (16 flags per thread and pass)
@@ -662,11 +667,17 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
     }
     const uint64_t e = s_end;
     for (uint64_t i = s + tid; i < e; i += blockDim.x) {
-      const uint32_t l2 = mirror ? (uint32_t)rev[rec[i].link] : rec[i].link;
-      atomicOr(&bm[l2 >> 5], 1u << (l2 & 31u));
+      const uint32_t l = rec[i].link;
+      if (doR) {
+        const uint32_t l2 = (uint32_t)rev[l];
+        atomicOr(&bmR[l2 >> 5], 1u << (l2 & 31u));
+      }
+      if (doA) atomicOr(&bmA[l >> 5], 1u << (l & 31u));
     }
     __syncthreads();
-    if (tid < 32) {  // exclusive prefix of the bitmap word counts
+    // exclusive prefix of the bitmap word counts: warp 0 the RS side, warp 1 (or 0) the AG side
+    if ((doR && warp == 0u) || (doA && warp == (doR ? 1u : 0u))) {
+      uint32_t *bm = (doR && warp == 0u) ? bmR : bmA, *pre = (doR && warp == 0u) ? preR : preA;
       uint32_t running = 0;
       for (uint32_t b = 0; b < nbw; b += 32u) {
         const uint32_t i = b + lane;
@@ -682,19 +693,33 @@ __global__ void rs_uniform_emit_kernel(const Rec *__restrict__ rec, uint64_t M, 
       }
     }
     __syncthreads();
-    const uint64_t base = mirror ? M - e : s;
+    Send32 *outA = mirror == 2u ? out + M : out;
     for (uint64_t i = s + tid; i < e; i += blockDim.x) {
       const Rec r = rec[i];
-      const uint32_t l2 = mirror ? (uint32_t)rev[r.link] : r.link;
-      const uint32_t rank = pre[l2 >> 5] + __popc(bm[l2 >> 5] & ((1u << (l2 & 31u)) - 1u));
-      Send32 o;
-      o.chunk = r.chunk;
-      o.link = l2;
-      o.src = src[l2];
-      o.dst = dst[l2];
-      o.t0 = mirror ? T_rs - (r.t_start + w0) : r.t_start + T_rs;
-      o.t1 = mirror ? T_rs - r.t_start : r.t_start + w0 + T_rs;
-      out[base + rank] = o;
+      if (doR) {
+        const uint32_t l2 = (uint32_t)rev[r.link];
+        const uint32_t rank = preR[l2 >> 5] + __popc(bmR[l2 >> 5] & ((1u << (l2 & 31u)) - 1u));
+        Send32 o;
+        o.chunk = r.chunk;
+        o.link = l2;
+        o.src = src[l2];
+        o.dst = dst[l2];
+        o.t0 = T_rs - (r.t_start + w0);
+        o.t1 = T_rs - r.t_start;
+        out[M - e + rank] = o;
+      }
+      if (doA) {
+        const uint32_t l = r.link;
+        const uint32_t rank = preA[l >> 5] + __popc(bmA[l >> 5] & ((1u << (l & 31u)) - 1u));
+        Send32 o;
+        o.chunk = r.chunk;
+        o.link = l;
+        o.src = src[l];
+        o.dst = dst[l];
+        o.t0 = r.t_start + T_rs;
+        o.t1 = r.t_start + w0 + T_rs;
+        outA[s + rank] = o;
+      }
     }
     __syncthreads();
   }
@@ -719,7 +744,7 @@ int launch_rs_uniform_emit(const Rec *rec, uint64_t M, const uint32_t *src, cons
   int rc = check_launch("seg_starts_kernel");
   if (rc) return rc;
   const uint32_t nbw = (L + 31u) / 32u;
-  const uint32_t smem = 2u * nbw * 4u;  // link-id bitmap + its prefix
+  const uint32_t smem = (mirror == 2u ? 4u : 2u) * nbw * 4u;  // link-id bitmap(s) + prefix(es)
   if (smem > 48u * 1024u) {
     const cudaError_t e = cudaFuncSetAttribute(rs_uniform_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {

@@ -375,11 +375,12 @@ def test_literal_custom_replacement(T):
     assert_parity(syn, sch, "CUSTOM")
 
 
-@pytest.mark.parametrize("q", [2, 4, 8])
+@pytest.mark.parametrize("q", [2, 4, 8, 11, 16])
 @pytest.mark.parametrize("case", ["uni4", "torus4x4", "hetero_mesh8x8", "torus8x8x8_k1"])
 def test_forced_cluster_splits(T, monkeypatch, q, case):
     """Every cluster size on small and large topologies, including splits with one NPU per CTA
-    (uni ring 4 at Q = 4) and CTAs that own no NPU at all (Q = 8 on 4 NPUs)."""
+    (uni ring 4 at Q = 4), CTAs that own no NPU at all (Q = 8 on 4 NPUs) and the non-portable
+    cluster sizes above 8 (11, 16)."""
     topo, k, coll, seeds = {
         "uni4": (W.uni_ring(4), 1, "AG", 5),
         "torus4x4": (W.torus([4, 4]), 2, "AR", 6),
@@ -420,7 +421,7 @@ def test_windowed_loop_parity(T, monkeypatch, name, win_ev):
     assert plan.info()["n_jobs"] >= seeds
 
 
-@pytest.mark.parametrize("q", [1, 3, 8])
+@pytest.mark.parametrize("q", [1, 3, 8, 12])
 def test_windowed_loop_cluster_sizes(T, monkeypatch, q):
     monkeypatch.setenv("TACOS_CLUSTER", str(q))
     syn, sch, _ = run_both(T, W.mesh2d(16, 16, 200, 100), 8, 128 << 10, "AR", 3)

@@ -1,6 +1,6 @@
 """Small synthesis cases for compute-sanitizer (memcheck / racecheck / synccheck), each
 checked against the oracle: configs 1-2, forced cluster splits Q = 2 / 4 / 8 (DSMEM mirror
-pushes, cluster barriers), the paper-literal kernel (f1), a relay collective (f2), the
+pushes, cluster barriers), the lock-step loop, the paper-literal kernel (f1), a relay collective (f2), the
 global-row (config-4 shape) path and the RS sort / uniform emitters.
 usage: python tools/sanitize_cases.py [quick]"""
 import os
@@ -20,6 +20,10 @@ CASES = [
     ("mesh8x16_k64_global_rows", {}, "W.mesh2d(8, 16, 200, 100)", "AR", 64, 2, {}),
     ("rand_asym_rs", {}, "W.random_strongly_connected(9, 20, 5, bws=(25, 50, 100), alphas=(0, 500))", "RS", 2, 3, {}),
     ("literal_torus4x4", {}, "W.torus([4, 4])", "AR", 2, 3, {"literal": True}),
+    # lock-step loop: double-buffered rows pushed as 16-byte DSMEM stores, compact link state
+    ("lockstep_torus8x8x8_q2", {}, "W.torus([8, 8, 8])", "AR", 1, 3, {}),
+    ("lockstep_uni_ring9_q3", {"TACOS_CLUSTER": "3"}, "W.uni_ring(9)", "AR", 3, 3, {}),
+    ("lockstep_torus4x4_q8", {"TACOS_CLUSTER": "8"}, "W.torus([4, 4])", "AG", 2, 3, {}),
     ("scatter_mesh6", {}, "W.mesh2d(6, 6)", "SCATTER", 1, 3, {"root": 2}),
 ]
 
