@@ -1,6 +1,6 @@
 """Randomized GPU-vs-oracle parity sweep (not part of the test suite): random strongly
-connected graphs, costs, chunk counts, collectives, variants (link-first, literal, relays,
-windowed wide rows) and forced cluster sizes; every mismatch is printed with its instance.
+connected graphs, costs, chunk counts, collectives, variants (link-first, one link cost =
+lock-step loop, literal, relays, windowed wide rows) and forced cluster sizes (1-16); every mismatch is printed with its instance.
 usage: python tools/stress_parity.py [N_CASES] [SEED]"""
 import os
 import sys
@@ -21,11 +21,13 @@ done = {}
 skipped = 0
 t0 = time.time()
 for case in range(n_cases):
-    mode = rng.choice(["plain", "plain", "wide", "literal", "relay", "custom"])
+    mode = rng.choice(["plain", "plain", "uniform", "wide", "literal", "relay", "custom"])
     n = int(rng.integers(3, 24 if mode != "wide" else 14))
     m = int(rng.integers(n, min(n * (n - 1), 4 * n) + 1))
     alphas = tuple(int(x) for x in rng.integers(0, 20000, size=int(rng.integers(1, 5))))
     bws = tuple(int(x) for x in rng.choice([25, 50, 100, 200, 400], size=int(rng.integers(1, 4))))
+    if mode == "uniform":  # one link cost: the lock-step loop (in-degree <= 8, <= 512 chunks)
+        alphas, bws = alphas[:1], bws[:1]
     topo = W.random_strongly_connected(n, m, int(rng.integers(0, 2**31)), bws=bws, alphas=alphas)
     k = int(rng.integers(1, 6)) if mode != "wide" else -(-1100 // n) + int(rng.integers(0, 30))
     seeds = int(rng.integers(1, 6))
@@ -34,7 +36,7 @@ for case in range(n_cases):
     nbytes = int(rng.choice([4096, 65536, 1 << 20]))
     env = {}
     if rng.random() < 0.3:
-        env["TACOS_CLUSTER"] = str(int(rng.integers(1, 9)))
+        env["TACOS_CLUSTER"] = str(int(rng.integers(1, 17)))
     if mode == "wide" and rng.random() < 0.5:
         env["TACOS_WIN_EV"] = str(int(rng.choice([1, 2, 5])))
     kw, okw = {}, {}
