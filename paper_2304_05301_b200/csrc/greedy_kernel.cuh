@@ -56,9 +56,6 @@ constexpr bool kP1Smem = true;
 #ifndef TACOS_STEP1  // 1: the P == 1 walk step keeps per-word counts and selects the bit without POPC
 #define TACOS_STEP1 1  // measured: config 2 0.283 -> 0.269 ms, config 3 0.745 -> 0.740, config 5 3.044 -> 3.015
 #endif
-#ifndef TACOS_WALK_UNROLL  // 1: the one-lane register walk unrolled over the slot count (experiment)
-#define TACOS_WALK_UNROLL 0
-#endif
 #ifndef TACOS_MIN_BLOCKS  // resident CTAs per SM the register budget is sized for
 #define TACOS_MIN_BLOCKS 1
 #endif
@@ -1368,34 +1365,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int v = 0; v < V; ++v) hv[v] = have4[v];
           }
-#if TACOS_WALK_UNROLL
-          // the walk unrolled over the slot count: current and prefetched rows alternate between
-          // two register sets (no per-step copies)
-          auto walk = [&](auto degc) {
-            constexpr int D = decltype(degc)::value;
-            uint4 ra[V], rb[V];
-            uint32_t pka = pick[b0 + (ordp & 15u)], pkb = 0;  // the pick draw travels with the row
-            load_row(b0 + (ordp & 15u), ra);
-#pragma unroll
-            for (int s = 0; s < D; ++s) {
-              if ((uint32_t)s >= nlive) break;
-              uint4(&cv)[V] = (s & 1) ? rb : ra;
-              uint4(&nx)[V] = (s & 1) ? ra : rb;
-              const uint32_t pk = (s & 1) ? pkb : pka;
-              const uint32_t p = b0 + ((ordp >> (4u * s)) & 15u);
-              if ((uint32_t)s + 1u < nlive) {
-                const uint32_t pn = b0 + ((ordp >> (4u * s + 4u)) & 15u);
-                load_row(pn, nx);
-                if (s & 1) pka = pick[pn];
-                else pkb = pick[pn];
-              }
-              step_row(p, pk, cv);
-            }
-          };
-          (void)nxt;
-          if (deg <= 6u) walk(std::integral_constant<int, 6>());
-          else walk(std::integral_constant<int, kRegDeg>());
-#else
           load_row(b0 + (ordp & 15u), nxt);
           uint32_t pk_nxt = pick[b0 + (ordp & 15u)];  // the pick draw travels with the row prefetch
           for (uint32_t s = 0; s < nlive; ++s) {
@@ -1411,7 +1380,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
             }
             step_row(p, pk, cv);
           }
-#endif
           if (job.trace != nullptr) {
             atomicMax(&s_dbg[2], (unsigned)(dbg_pro - pm_t0));
             atomicMax(&s_dbg[3], (unsigned)(clock64() - dbg_pro));
