@@ -31,6 +31,17 @@
 // CTA through distributed shared memory; the delivered count, the next event
 // time and the record bitmap are exchanged with DSMEM atomics; the two
 // event-level barriers become cluster barriers (release/acquire at cluster scope).
+//
+// Three event loops share the phases above:
+//   per-event  the scheme above;
+//   lock-step  one link cost, one lane per destination: every send started at t
+//              ends at the next event t + w, so a walker writes d's next held row
+//              (= have[d] after its walk) into the other buffer of held[2][N] and
+//              pushes it to the mirroring CTAs -- no PA, one cluster barrier per
+//              event; records in (t_start, CTA, position) order from a position
+//              bitmap, ranked by link at emission;
+//   windowed   several link costs, wide rows: all events of [T0, T0 + w_min)
+//              run per destination between one set of cluster barriers.
 #pragma once
 #include <cooperative_groups.h>
 
