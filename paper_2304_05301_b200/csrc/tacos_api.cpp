@@ -378,11 +378,15 @@ extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_
   t->bw.assign(bw, bw + n_links);
   // (src, dst) -> link id: open addressing, linear probing, load <= 1/2
   size_t cap = 16;
-  while (cap < (size_t)n_links * 2) cap <<= 1;
+  uint32_t lg = 4;
+  while (cap < (size_t)n_links * 2) {
+    cap <<= 1;
+    ++lg;
+  }
   std::vector<uint64_t> hkey(cap, ~0ull);
   std::vector<int32_t> hval(cap, -1);
-  auto slot_of = [&](uint64_t key) {
-    size_t h = (size_t)((key * 0x9E3779B97F4A7C15ull) >> 20) & (cap - 1);
+  auto slot_of = [&](uint64_t key) {  // Fibonacci hashing: the top lg bits of the product
+    size_t h = (size_t)((key * 0x9E3779B97F4A7C15ull) >> (64u - lg));
     while (hkey[h] != ~0ull && hkey[h] != key) h = (h + 1) & (cap - 1);
     return h;
   };
