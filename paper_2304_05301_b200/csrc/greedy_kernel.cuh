@@ -183,7 +183,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   // next event themselves into the other held buffer (held[2][N], event parity) and an event needs
   // one cluster barrier.  Its layout keeps only the CTA's own have rows and in-link positions:
   // the pointers are shifted so that global indices address them.
-  constexpr bool kLock = REG_PATH && P == 1 && kP1Smem && ROWS_SMEM && LINKS_SMEM && !MASKED;
+  constexpr bool kLock = P == 1 && kP1Smem && ROWS_SMEM && LINKS_SMEM && !MASKED;
   const bool lockstep = kLock && lay.lockstep != 0u;
   uint32_t *const held_base = held, *const hver_base = hver;
   if (lockstep) {
@@ -1144,8 +1144,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           mo_w = wp < mo_w ? wp : mo_w;
           ++myM;
           ++my_claims;
-          if (lockstep) {  // position bits, set once per destination after the walk
-            pmask |= 1u << (p - b0);
+          if (lockstep) {  // position bits, set once per destination after the walk (in-degree <= 32)
+            if (REG_PATH || deg <= 32u) pmask |= 1u << (p - b0);  // (register path: in-degree <= 8)
+            else atomicOr(&bm[(p - p_lo) >> 5], 1u << ((p - p_lo) & 31u));
           } else {
             const uint32_t lid = t_lid[p];
             atomicOr(&bm[lid >> 5], 1u << (lid & 31u));
@@ -1248,6 +1249,36 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
         };
 
         // REG_PATH (every in-degree <= kRegDeg): ranks in registers; else shared memory
+        // lock-step loop: d's held row at the next event = have[d] after the walk (at t every
+        // earlier send has arrived, so have == held; the claims of t arrive at t + w, the next
+        // event), written to the other held buffer and pushed to the CTAs that mirror d
+        auto ls_push = [&](bool arrived) {
+          const uint32_t nb = (e + 1u) & 1u;
+          uint4 *hn = reinterpret_cast<uint4 *>(held_base + ((size_t)nb * N + d) * Wr);
+          uint32_t *hvn = hver_base + (size_t)nb * N + d;
+          uint4 r[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) r[v] = have4[v];
+#pragma unroll
+          for (int v = 0; v < V; ++v) hn[v] = r[v];
+          const uint32_t ver = arrived ? e + 1u : hver[d];
+          *hvn = ver;
+          if (Q > 1)
+            for (uint32_t pm = s_peers[d]; pm; pm &= pm - 1u) {
+              const uint32_t rk = __ffs(pm) - 1u;
+#pragma unroll
+              for (int v = 0; v < V; ++v) dsmem_st_v4(dsmem_addr(hn + v, rk), r[v]);
+              dsmem_st_u32(dsmem_addr(hvn, rk), ver);
+            }
+        };
+        // lock-step loop: this event's matched positions (bit q - p_lo of the CTA's position
+        // bitmap; in-degree > 32 sets them per match): the records are written in position order,
+        // ranked by link at emission
+        auto ls_positions = [&]() {
+          const uint32_t o = b0 - p_lo, sh = o & 31u;
+          if (pmask) atomicOr(&bm[o >> 5], pmask << sh);
+          if (sh != 0u && (pmask >> (32u - sh)) != 0u) atomicOr(&bm[(o >> 5) + 1u], pmask >> (32u - sh));
+        };
         if constexpr (REG_PATH && P == 1 && kP1Smem) {
           // ---- one thread per destination: in-link j in slot j (static), ranks by pairwise
           //      comparisons, walk order packed 4 bits per rank, and the next in-link's source
@@ -1336,28 +1367,6 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
 #pragma unroll
             for (int j = 0; j < D; ++j) ordp |= (uint32_t)j << (4u * rk[j]);
           };
-          // lock-step loop: d's held row at the next event = have[d] after the walk (at t every
-          // earlier send has arrived, so have == held; the claims of t arrive at t + w, the next
-          // event), written to the other held buffer and pushed to the CTAs that mirror d
-          auto ls_push = [&](bool arrived) {
-            const uint32_t nb = (e + 1u) & 1u;
-            uint4 *hn = reinterpret_cast<uint4 *>(held_base + ((size_t)nb * N + d) * Wr);
-            uint32_t *hvn = hver_base + (size_t)nb * N + d;
-            uint4 r[V];
-#pragma unroll
-            for (int v = 0; v < V; ++v) r[v] = have4[v];
-#pragma unroll
-            for (int v = 0; v < V; ++v) hn[v] = r[v];
-            const uint32_t ver = arrived ? e + 1u : hver[d];
-            *hvn = ver;
-            if (Q > 1)
-              for (uint32_t pm = s_peers[d]; pm; pm &= pm - 1u) {
-                const uint32_t rk = __ffs(pm) - 1u;
-#pragma unroll
-                for (int v = 0; v < V; ++v) dsmem_st_v4(dsmem_addr(hn + v, rk), r[v]);
-                dsmem_st_u32(dsmem_addr(hvn, rk), ver);
-              }
-          };
           const uint32_t claims0 = my_claims;
           if (deg <= 6u) prologue(std::integral_constant<int, 6>());
           else prologue(std::integral_constant<int, kRegDeg>());
@@ -1402,11 +1411,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
           if (lockstep) {
             ls_push(my_claims != claims0);
-            // this event's matched positions (bit q - p_lo of the CTA's position bitmap): the
-            // records are written in position order, ranked by link at emission
-            const uint32_t o = b0 - p_lo, sh = o & 31u;
-            if (pmask) atomicOr(&bm[o >> 5], pmask << sh);
-            if (sh != 0u && (pmask >> (32u - sh)) != 0u) atomicOr(&bm[(o >> 5) + 1u], pmask >> (32u - sh));
+            ls_positions();
           }
         } else if constexpr (REG_PATH && P <= 2) {
           // ---- a group of P lanes per destination: every lane ranks the in-links itself
@@ -1738,8 +1743,12 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           myD += nfree ? 1u : 0u;
         }
         if (gl == 0) myL += nl;
-        if (nl == 0u) continue;
+        if (nl == 0u) {
+          if (lockstep) ls_push(false);
+          continue;
+        }
         if constexpr (P == 1) {
+          const uint32_t claims0 = my_claims;
           // one lane per destination: the walk takes the live in-links in shorter-link-first order
           // (R3: smallest (w, u_ord, position) first, positions ascend with the link id) by a
           // selection over the compact live list -- O(live^2) instead of O(live x in-degree)
@@ -1765,6 +1774,10 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
           }
 #pragma unroll
           for (int v = 0; v < V; ++v) if (!kHaveSmem) have4[v] = hv[v];
+          if (lockstep) {
+            ls_push(my_claims != claims0);
+            ls_positions();
+          }
           continue;
         }
         if (P > 1) __syncwarp(gmask);
@@ -1826,7 +1839,7 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
       // (with the worklist only the active destinations were walked: full pass)
       const bool walk_min = kWalkMin || worklist;
       uint32_t mo = walk_min ? mo_w : ~0u;
-      if (!walk_min)
+      if (!walk_min && !lockstep)
       for (uint32_t p = p_lo + tid; p < p_hi; p += nthr)
         if (cur[p] != kNone) {
           const uint32_t o = (uint32_t)(busy[p] - t);

@@ -906,11 +906,11 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         lq = l2;
       }
       // Lock-step loop (greedy_kernel.cuh): one link cost per topology, one lane per
-      // destination on the register path, AG-type problem without relays: every send started at t
+      // destination (register or shared-memory ranking path), AG-type problem without relays: every send started at t
       // ends at the next event t + w, so the walkers write the arrivals themselves (held rows
       // double-buffered by event parity) and an event needs one cluster barrier.  TACOS_LOCKSTEP=0: off.
       const char *env_ls = getenv("TACOS_LOCKSTEP");
-      if (!win && !multi_w && P0 == 1u && lq.reg_path && !relay && !custom && !(p->flags & TACOS_FLAG_LITERAL) &&
+      if (!win && !multi_w && P0 == 1u && !relay && !custom && !(p->flags & TACOS_FLAG_LITERAL) &&
           !lq.worklist && (!env_ls || atoi(env_ls) != 0)) {
         const uint32_t Q = lq.cluster;
         uint32_t pos_cap = 0;
@@ -923,7 +923,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
               pos_cap = std::max(pos_cap, tt->in_ptr[o][hi] - tt->in_ptr[o][lo]);
             }
         }
-        add_lockstep(lq, maxN, std::max(pos_cap, 1u), smem_limit);
+        add_lockstep(lq, maxN, maxL, std::max(pos_cap, 1u), smem_limit);
       }
     };
     finish_layout(g.lay);

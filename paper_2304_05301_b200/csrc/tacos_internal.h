@@ -101,7 +101,7 @@ constexpr uint32_t kWinBits = 16384;  // window length cap (bitmap of event offs
 void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg);
 // Switch a one-lane shared-memory layout to the lock-step loop's (pos_cap = the most in-link
 // positions a CTA of the cluster owns); false (layout unchanged) when it does not fit.
-bool add_lockstep(Layout &lay, uint32_t N, uint32_t pos_cap, size_t smem_limit);
+bool add_lockstep(Layout &lay, uint32_t N, uint32_t L, uint32_t pos_cap, size_t smem_limit);
 
 // q_force: cluster size to use (0: the automatic choice; TACOS_CLUSTER overrides both)
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,

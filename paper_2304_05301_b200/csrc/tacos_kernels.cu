@@ -144,10 +144,14 @@ void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg) {
   lay.smem_bytes = s;
 }
 
-bool add_lockstep(Layout &lay, uint32_t N, uint32_t pos_cap, size_t smem_limit) {
+bool add_lockstep(Layout &lay, uint32_t N, uint32_t L, uint32_t pos_cap, size_t smem_limit) {
   auto al = [](uint32_t x, uint32_t a) { return (x + a - 1u) / a * a; };
-  if (!lay.rows_in_smem || !lay.links_in_smem || lay.window || lay.pre_draw) return false;
+  // everything in shared memory (u16 NPU / link ids): the compact layout may fit where the
+  // full one put the rows in global memory
+  if (N >= 65536u || L >= 65536u || lay.window || lay.pre_draw) return false;
   Layout l = lay;
+  l.rows_in_smem = 1u;
+  l.links_in_smem = 1u;
   const uint32_t Q = l.cluster, n_own = (N + Q - 1u) / Q, Lc = pos_cap;
   l.rows_bytes = al((2u * N + n_own) * l.row_stride * 4u, 16u);  // held[2][N], have[n_own]
   uint32_t o = 0;

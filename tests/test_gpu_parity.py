@@ -521,24 +521,30 @@ def _lockstep_case(name):
         "uni_ring9_ar": (W.uni_ring(9), 3, "AR", 4),  # asymmetric: RS searched on G^T (sigma 1 jobs)
         "hypercube6_k2_ar": (W.hypercube(6), 2, "AR", 4),
         "mesh6x5_uniform_ar": (W.mesh2d(6, 5, 100, 100), 2, "AR", 4),  # border NPUs: in-degree 2 to 4
+        # in-degree > 8: the shared-memory ranking path; > 32: position bits set per match
+        "fc12_k2_ar": (W.fully_connected(12), 2, "AR", 5),
+        "hypercube9_ar": (W.hypercube(9), 1, "AR", 3),
+        "fc40_ag": (W.fully_connected(40), 1, "AG", 4),
     }[name]
 
 
 @pytest.mark.parametrize("q", ["", "1", "2", "3", "8"])
 @pytest.mark.parametrize("name", ["torus8x8x8_k1_ar", "torus4x4_k2_ar", "torus8x8_k4_ag", "torus8x8_k4_rs",
-                                  "uni_ring9_ar", "hypercube6_k2_ar", "mesh6x5_uniform_ar"])
+                                  "uni_ring9_ar", "hypercube6_k2_ar", "mesh6x5_uniform_ar", "fc12_k2_ar",
+                                  "hypercube9_ar", "fc40_ag"])
 def test_lockstep_loop_parity(T, monkeypatch, name, q):
     topo, k, coll, seeds = _lockstep_case(name)
     if q:
         monkeypatch.setenv("TACOS_CLUSTER", q)
     syn, sch, t = run_both(T, topo, k, 1 << 20, coll, seeds)
     assert_parity(syn, sch, coll)
-    # (one CTA cannot hold the 512-NPU torus's double-buffered rows: the per-event loop then)
-    fits = not (name == "torus8x8x8_k1_ar" and q == "1")
+    # (one CTA cannot hold the 512-NPU torus's or hypercube's double-buffered rows: the per-event
+    # loop then)
+    fits = not (name in ("torus8x8x8_k1_ar", "hypercube9_ar") and q == "1")
     assert T.Plan(t, coll, k, 1 << 20, seeds).info()["event_loop"] == (2 if fits else 0)
 
 
-@pytest.mark.parametrize("name", ["torus8x8x8_k1_ar", "uni_ring9_ar", "torus8x8_k4_ag"])
+@pytest.mark.parametrize("name", ["torus8x8x8_k1_ar", "uni_ring9_ar", "torus8x8_k4_ag", "fc12_k2_ar", "fc40_ag"])
 def test_lockstep_equals_per_event_loop(T, monkeypatch, name):
     """Same schedules, times and counters with the lock-step loop off (TACOS_LOCKSTEP=0)."""
     topo, k, coll, seeds = _lockstep_case(name)
