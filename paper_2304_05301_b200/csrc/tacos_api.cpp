@@ -156,7 +156,7 @@ struct tacos_topology {
   bool strongly_connected = false;
   // orientation 0 = G (grouped by dst), 1 = G^T (grouped by src)
   std::vector<uint32_t> in_ptr[2], pos_lid[2], pos_src[2], pos_dst[2];
-  int device = -1;  // device current at load time (its copy is uploaded eagerly), -1 without a GPU
+  int device = -1;  // device current at load time, -1 without a GPU
   // per-device copies of the CSR arrays (tacos_synthesize with n_devices > 1 uses several),
   // created on first use under the mutex; the handle stays logically immutable
   struct Dev {
@@ -166,6 +166,8 @@ struct tacos_topology {
     uint32_t *d_src = nullptr, *d_dst = nullptr;
     int32_t *d_rev = nullptr;
     std::vector<DevBuf> bufs;
+    DevBuf stage;               // pinned staging block of the upload (kept until the handle is freed)
+    cudaEvent_t ready = nullptr;  // recorded after the upload on the stream of the first user
   };
   mutable std::mutex mu;
   mutable std::vector<std::unique_ptr<Dev>> devs;
@@ -177,6 +179,8 @@ struct tacos_topology {
     for (auto &d : devs) {
       if (cudaSetDevice(d->dev) == cudaSuccess) cudaDeviceSynchronize();
       for (auto &b : d->bufs) device_pool().release(b.dev, b.p, b.cls);
+      if (d->stage.p) pinned_pool().release(d->stage.dev, d->stage.p, d->stage.cls);
+      if (d->ready) cudaEventDestroy(d->ready);
     }
     if (have_cur) cudaSetDevice(cur);
     cudaGetLastError();
@@ -186,8 +190,9 @@ using TopoDev = tacos_topology::Dev;
 
 namespace {
 // The topology's arrays on device `dev` (the calling thread's current device), uploaded on
-// first use (one pinned staging copy + one H2D copy, synchronous).
-int topo_on_device(const tacos_topology *t, int dev, const TopoDev **out);
+// first use: one pinned staging copy + one H2D copy on `st`, not waited for; later users on
+// other streams wait for it (event), so nothing here synchronizes.
+int topo_on_device(const tacos_topology *t, int dev, const TopoDev **out, cudaStream_t st);
 }  // namespace
 
 namespace {
@@ -234,16 +239,17 @@ struct Stager {
     return TACOS_OK;
   }
   void put(size_t off, const void *h, size_t bytes) { parts.push_back(Part{h, off, bytes}); }
-  // one pinned staging copy + one H2D copy; synchronizes the stream (the staging block is returned)
-  int copy_sync(int dev, cudaStream_t st) {
+  // one pinned staging copy + one H2D copy on `st`, an event recorded after it; the pinned
+  // block is handed to the caller (released once the copy is known complete)
+  int copy_async(int dev, cudaStream_t st, DevBuf *stage, cudaEvent_t *ev) {
     if (total == 0) return TACOS_OK;
-    size_t cls = 0;
-    void *h = pinned_pool().alloc(dev, total, &cls);
-    if (!h) return fail(TACOS_E_NOMEM, "pinned allocation of %zu bytes failed", total);
-    for (const Part &q : parts) std::memcpy(reinterpret_cast<unsigned char *>(h) + q.off, q.h, q.bytes);
-    cudaError_t e = cudaMemcpyAsync(d_base, h, total, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    pinned_pool().release(dev, h, cls);
+    stage->dev = dev;
+    stage->p = pinned_pool().alloc(dev, total, &stage->cls);
+    if (!stage->p) return fail(TACOS_E_NOMEM, "pinned allocation of %zu bytes failed", total);
+    for (const Part &q : parts) std::memcpy(reinterpret_cast<unsigned char *>(stage->p) + q.off, q.h, q.bytes);
+    cudaError_t e = cudaMemcpyAsync(d_base, stage->p, total, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(*ev, st);
     if (e != cudaSuccess) return fail(TACOS_E_CUDA, "staged upload: %s", cudaGetErrorString(e));
     return TACOS_OK;
   }
@@ -312,10 +318,11 @@ bool symmetric_for(const tacos_topology *t, const std::vector<uint32_t> &w) {
 }  // namespace
 
 namespace {
-int topo_on_device(const tacos_topology *t, int dev, const TopoDev **out) {
+int topo_on_device(const tacos_topology *t, int dev, const TopoDev **out, cudaStream_t st) {
   std::lock_guard<std::mutex> g(t->mu);
   for (auto &d : t->devs)
     if (d->dev == dev) {
+      if (d->ready) CUDA_TRY(cudaStreamWaitEvent(st, d->ready, 0));
       *out = d.get();
       return TACOS_OK;
     }
@@ -352,8 +359,9 @@ int topo_on_device(const tacos_topology *t, int dev, const TopoDev **out) {
   d->d_src = sg.at<uint32_t>(o_s);
   d->d_dst = sg.at<uint32_t>(o_d);
   d->d_rev = sg.at<int32_t>(o_r);
-  if ((rc = sg.copy_sync(dev, nullptr))) {
+  if ((rc = sg.copy_async(dev, st, &d->stage, &d->ready))) {
     for (auto &b : d->bufs) device_pool().release(b.dev, b.p, b.cls);
+    if (d->stage.p) pinned_pool().release(d->stage.dev, d->stage.p, d->stage.cls);
     return rc;
   }
   *out = d.get();
@@ -429,16 +437,11 @@ extern "C" int tacos_load_topology(int32_t n_npus, int32_t n_links, const int32_
   }
   t->strongly_connected = reach_all(n_npus, t->in_ptr[0], t->pos_src[0]) && reach_all(n_npus, t->in_ptr[1], t->pos_src[1]);
 
+  // (the device copy is made by the first plan that uses the topology, on its stream)
   int dev = -1;
   int n = 0;
-  if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) {
-    t->device = dev;
-    const TopoDev *td = nullptr;
-    int rc = topo_on_device(t.get(), dev, &td);
-    if (rc) return rc;
-  } else {
-    cudaGetLastError();
-  }
+  if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) t->device = dev;
+  else cudaGetLastError();
   *out = t.release();
   return TACOS_OK;
 }
@@ -757,7 +760,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
     if (!t) return fail(TACOS_E_INVALID_ARG, "null topology %u", i);
     Part &pt = pl->parts[i];
     pt.topo = t;
-    if ((rc = topo_on_device(t, dev, &pt.td))) return rc;
+    if ((rc = topo_on_device(t, dev, &pt.td, st))) return rc;
     pt.N = (uint32_t)t->N;
     pt.L = (uint32_t)t->L;
     pt.custom = custom;
