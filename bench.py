@@ -381,9 +381,12 @@ def run_gpu(args):
         "smem_pipe_frac": ncu.get("smem_pipe_frac"), "issue_active_pct": ncu.get("issue_active_pct"),
         "warps_active_pct": ncu.get("warps_active_pct"), "ncu_source": ncu.get("source"),
         "grid": {"ctas": info["ctas"], "sms": n_sms, "cluster": info["cluster"], "threads": info["threads"],
-                 "smem_bytes": info["smem_bytes"], "rows_bytes_global": info["rows_bytes"]},
-        "limiter": ("latency: per-event dependent walks of each destination and two cluster barriers per event "
-                    "(DESIGN.md §5); neither HBM nor the shared-memory pipe is saturated") if info["rows_in_smem"] else
+                 "smem_bytes": info["smem_bytes"], "rows_bytes_global": info["rows_bytes"],
+                 "event_loop": {0: "per-event", 1: "windowed", 2: "lock-step"}.get(info.get("event_loop"), "?")},
+        "limiter": ("latency: per-event dependent walks of each destination and "
+                    + ("one cluster barrier per event (lock-step loop" if info.get("event_loop") == 2
+                       else "two cluster barriers per event (per-event loop")
+                    + ", DESIGN.md §5); neither HBM nor the shared-memory pipe is saturated") if info["rows_in_smem"] else
                    ("latency: L2 round trips of the 1 KiB source rows in the windowed loop and three cluster barriers "
                     "per window (DESIGN.md §5); rows are " + ("L2-resident" if info["rows_bytes"] < 126e6 else
                                                               "larger than L2") + ", DRAM traffic is the send records"),
