@@ -555,3 +555,30 @@ def test_lockstep_equals_per_event_loop(T, monkeypatch, name):
     b = T.synthesize(t, coll, k, 1 << 20, seeds, keep_seed_times=True)
     assert a.sends.tobytes() == b.sends.tobytes() and a.result == b.result
     assert np.array_equal(a.seed_times, b.seed_times)
+
+
+def test_topology_first_use_on_side_streams(T):
+    """The topology's device copy is made by its first plan on that plan's stream (no
+    synchronous upload at load time); a later plan on another stream waits for it.  Fresh
+    topologies used first on non-blocking side streams, the default stream busy meanwhile,
+    then reused on a second stream: the oracle's schedule every time."""
+    import torch
+
+    wl = W.config(2)
+    syn = oracle.synthesize(wl.topo, 4, 1 << 20, "AR", list(range(3)))
+    busy = torch.empty(1 << 26, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        t = T.Topology.from_workload_topology(wl.topo)
+        p, keep = T.make_params("AR", 4, 1 << 20, 3)
+        n = T.max_sends(t, p)
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        outs = []
+        for st in (s1, s2):
+            busy.fill_(1)  # work queued on the default stream
+            host = torch.zeros(n * 32, dtype=torch.uint8).pin_memory()
+            r = T.synthesize_into(t, p, host.data_ptr(), n, st.cuda_stream)
+            assert r["T"] == syn.T and r["seed"] == syn.seed and r["n_sends"] == n
+            outs.append(host.numpy().tobytes())
+        assert outs[0] == outs[1] == syn.sends.tobytes()
+        del t
+    torch.cuda.synchronize()
