@@ -289,9 +289,15 @@ bool reach_all(int32_t N, const std::vector<uint32_t> &ptr, const std::vector<ui
 // a1: w = ceil((alpha*bw + n) / (bw*f)) exactly (P:L104 alpha + n/bw; P:L172 ceil(l/f))
 int quantize(uint32_t alpha, uint32_t bw, uint64_t n, uint32_t f, uint32_t *w_out) {
   if (bw == 0) return TACOS_E_TOPOLOGY;
-  const unsigned __int128 num = (unsigned __int128)alpha * bw + n;
-  const unsigned __int128 den = (unsigned __int128)bw * (f ? f : 1u);
-  const unsigned __int128 q = num / den + (num % den != 0 ? 1 : 0);
+  const uint64_t ab = (uint64_t)alpha * bw, den64 = (uint64_t)bw * (f ? f : 1u);  // both < 2^64
+  unsigned __int128 q;
+  if (n <= ~0ull - ab) {  // the numerator fits 64 bits: the same quotient without 128-bit division
+    const uint64_t num64 = ab + n;
+    q = num64 / den64 + (num64 % den64 != 0 ? 1u : 0u);
+  } else {
+    const unsigned __int128 num = (unsigned __int128)ab + n;
+    q = num / den64 + (num % den64 != 0 ? 1 : 0);
+  }
   if (q == 0) return TACOS_E_TOPOLOGY;
   if (q >= 0xFFFFFFFFull) return TACOS_E_OVERFLOW;  // w < 2^32 - 1 (the search packs (w, u_ord) into 64 bits)
   *w_out = (uint32_t)q;
@@ -300,8 +306,20 @@ int quantize(uint32_t alpha, uint32_t bw, uint64_t n, uint32_t f, uint32_t *w_ou
 
 int link_costs(const tacos_topology *t, uint64_t n, uint32_t f, std::vector<uint32_t> &w) {
   w.resize(t->L);
+  uint32_t pa = 0, pb = 0, pw = 0;  // the previous link's (alpha, bw) and cost: uniform runs reuse it
+  bool have_prev = false;
   for (int32_t l = 0; l < t->L; ++l) {
+    if (have_prev && t->alpha[l] == pa && t->bw[l] == pb) {
+      w[l] = pw;
+      continue;
+    }
     int rc = quantize(t->alpha[l], t->bw[l], n, f, &w[l]);
+    if (rc == TACOS_OK) {
+      pa = t->alpha[l];
+      pb = t->bw[l];
+      pw = w[l];
+      have_prev = true;
+    }
     if (rc == TACOS_E_TOPOLOGY) return fail(rc, "link %d has zero cost (alpha = n = 0)", l);
     if (rc == TACOS_E_OVERFLOW) return fail(rc, "link %d cost exceeds 2^32 - 2 time units", l);
     if (rc) return fail(rc, "link %d: bad cost", l);

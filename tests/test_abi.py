@@ -162,3 +162,34 @@ def test_multi_device_entry_points_without_gpu(T):
         assert err.code == T.TACOS_E_NCCL
     else:
         assert v >= 20000
+
+
+def test_link_costs_wide_arithmetic(T):
+    """a1: w = ceil((alpha * bw + n) / (bw * f)) exactly, on both sides of the
+    64-bit numerator boundary (the library divides in 64 bits when alpha * bw + n fits, in 128
+    bits otherwise), with the error codes for w = 0 and w >= 2^32 - 1; the expected values are
+    the definition in Python integers."""
+    rng = np.random.default_rng(5)
+    M32, M64 = 2**32 - 1, 2**64 - 1
+    cases = []
+    for a in (0, 1, 7, M32, int(rng.integers(1, M32))):
+        for b in (1, 3, M32, int(rng.integers(1, M32))):
+            ab = a * b
+            for n in (0, 1, M64 - ab, min(M64, M64 - ab + 1), 2**63, M64, int(rng.integers(0, 2**63))):
+                if n > M64:
+                    continue
+                for f in (1, 2**31, M32):
+                    cases.append((a, b, n, f))
+    for a, b, n, f in cases:
+        t = T.Topology(2, [0, 1], [1, 0], [a, a], [b, b])
+        q = -(-(a * b + n) // (b * f))
+        if q == 0:
+            with pytest.raises(T.TacosError) as e:
+                t.link_costs(n, f)
+            assert e.value.code == T.TACOS_E_TOPOLOGY
+        elif q >= M32:
+            with pytest.raises(T.TacosError) as e:
+                t.link_costs(n, f)
+            assert e.value.code == T.TACOS_E_OVERFLOW
+        else:
+            assert t.link_costs(n, f).tolist() == [q, q], (a, b, n, f)
