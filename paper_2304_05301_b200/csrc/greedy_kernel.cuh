@@ -95,8 +95,13 @@ struct ThreadsFor {
 };
 // MASKED (relays, R22): candidates are also and-ed with the
 // per-position allow row, and only arrivals of chunks in post[dst] count.
-template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM, bool REG_PATH, bool MASKED>
-__global__ void __launch_bounds__(ThreadsFor<P, V>::value, TACOS_MIN_BLOCKS)
+// BIG: the one-lane four-vector register-path kernel bounded at kBigThreads (128 registers) for
+// CTAs with more own destinations than the default bound leaves walker threads for (e.g. 512 NPUs
+// on one SM): one destination per walker instead of two in sequence (the paper's 512-NPU
+// Ring x FC x Switch: 8.1 -> 7.0 ms); the default bound stays faster where the destinations fit.
+constexpr int kBigThreads = 512;
+template <int P, int V, bool ROWS_SMEM, bool LINKS_SMEM, bool REG_PATH, bool MASKED, bool BIG = false>
+__global__ void __launch_bounds__(BIG ? kBigThreads : ThreadsFor<P, V>::value, TACOS_MIN_BLOCKS)
 greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Layout lay) {
   static_assert(P >= 1 && P <= 32 && (P & (P - 1)) == 0, "P must be a power of two <= 32");
   // one thread per destination with shared-memory rows: `have` stays in shared memory and a
@@ -1947,9 +1952,9 @@ greedy_kernel(const Job *__restrict__ jobs, JobOut *__restrict__ outs, const Lay
   }
 }
 
-template <int P, int V, bool R, bool K, bool G, bool M = false>
+template <int P, int V, bool R, bool K, bool G, bool M = false, bool B = false>
 int launch_greedy_one(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobOut *d_outs, cudaStream_t st) {
-  auto fn = greedy_kernel<P, V, R, K, G, M>;
+  auto fn = greedy_kernel<P, V, R, K, G, M, B>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.smem_bytes);
   // clusters beyond the portable 8 CTAs (B200: up to 16) are opt-in per kernel
   if (e == cudaSuccess && lay.cluster > 8u) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -2025,6 +2030,9 @@ int launch_greedy_pv(const Layout &lay, const Job *d_jobs, uint32_t n_jobs, JobO
     return launch_greedy_one<P, V, false, false, false, true>(lay, d_jobs, n_jobs, d_outs, st);
   }
   if (lay.reg_path) {
+    if constexpr (P == 1 && V == 4)
+      if (lay.big && lay.rows_in_smem && lay.links_in_smem)
+        return launch_greedy_one<P, V, true, true, true, false, true>(lay, d_jobs, n_jobs, d_outs, st);
     if (lay.rows_in_smem && lay.links_in_smem) return launch_greedy_one<P, V, true, true, true>(lay, d_jobs, n_jobs, d_outs, st);
     if (lay.links_in_smem) return launch_greedy_one<P, V, false, true, true>(lay, d_jobs, n_jobs, d_outs, st);
     return launch_greedy_one<P, V, false, false, true>(lay, d_jobs, n_jobs, d_outs, st);

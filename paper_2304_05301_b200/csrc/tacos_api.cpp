@@ -946,6 +946,7 @@ int plan_build(const tacos_topology *const *topos, uint32_t n_topos, const tacos
         }
         add_lockstep(lq, maxN, maxL, std::max(pos_cap, 1u), smem_limit);
       }
+      if (lq.big && !(lq.reg_path && lq.rows_in_smem && lq.links_in_smem && !lq.masked)) layout_drop_big(lq);
     };
     finish_layout(g.lay);
     // Cluster size: the largest Q <= 8 (any size, not only powers of two) with jobs * Q <= #SMs,

@@ -93,6 +93,8 @@ struct Layout {
   // double-buffered by event parity (held[2][N], then the own have rows), link state of the
   // CTA's own in-link positions only (pos_cap per CTA), hver[2][N]
   uint32_t lockstep, pos_cap;
+  // 1: the one-lane four-vector register-path kernel with the larger thread bound (kBigThreads)
+  uint32_t big;
 };
 constexpr uint32_t kMaxCluster = 16;  // CTAs per job at most (non-portable cluster sizes above 8)
 constexpr uint32_t kWinEv = 256;      // events per window at most (a longer window is cut there)
@@ -102,6 +104,9 @@ void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg);
 // Switch a one-lane shared-memory layout to the lock-step loop's (pos_cap = the most in-link
 // positions a CTA of the cluster owns); false (layout unchanged) when it does not fit.
 bool add_lockstep(Layout &lay, uint32_t N, uint32_t L, uint32_t pos_cap, size_t smem_limit);
+// The larger-bound kernel exists for the register path with on-chip state only: otherwise back
+// to the default bound.
+void layout_drop_big(Layout &lay);
 
 // q_force: cluster size to use (0: the automatic choice; TACOS_CLUSTER overrides both)
 Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL, size_t smem_limit, uint32_t n_jobs,

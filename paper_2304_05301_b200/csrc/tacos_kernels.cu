@@ -105,11 +105,19 @@ Layout make_layout(uint32_t N, uint32_t L, uint32_t Wp, uint32_t P, uint32_t VPL
   // threads: one destination group per own destination in one pass when possible, plus
   // the warps that write the previous event's records meanwhile (about one thread per 16
   // own in-links; measured on configs 2, 3, 5)
-  const uint32_t th_max = VPL == 1 ? 768u : (P == 2 && VPL == 2) ? 640u
-                          : VPL == 2 ? (uint32_t)TACOS_V2_THREADS
-                          : P > 2u  ? (uint32_t)TACOS_WIDE_THREADS : (uint32_t)TACOS_V4_THREADS;  // = ThreadsFor<P, V>
+  uint32_t th_max = VPL == 1 ? 768u : (P == 2 && VPL == 2) ? 640u
+                    : VPL == 2 ? (uint32_t)TACOS_V2_THREADS
+                    : P > 2u  ? (uint32_t)TACOS_WIDE_THREADS : (uint32_t)TACOS_V4_THREADS;  // = ThreadsFor<P, V>
   const uint32_t walkers = (n_own * P + 31u) & ~31u;
   const uint32_t recw = std::max<uint32_t>(64u, ((L / Q) / 16u + 31u) & ~31u);
+  // one lane, four vectors, more own destinations than the default bound leaves walkers for: the
+  // larger-bound instantiation (register path with on-chip state only; the host clears `big` for
+  // the other paths, launch_greedy_pv), one destination per walker
+  lay.big = 0u;
+  if (P == 1u && VPL == 4u && walkers + 32u > th_max && !getenv("TACOS_NO_BIG")) {
+    lay.big = 1u;
+    th_max = (uint32_t)kBigThreads;
+  }
   uint32_t th = std::max<uint32_t>(128u, walkers + recw);
   if (th > th_max) th = th_max;
   if (th < P) th = P;
@@ -142,6 +150,11 @@ void add_window(Layout &lay, uint32_t N, uint32_t window, uint32_t deg) {
   lay.off_waoff = s; s += al(N * deg * 4u, 16u);
   lay.off_wachk = s; s += al(N * deg * 2u, 16u);
   lay.smem_bytes = s;
+}
+
+void layout_drop_big(Layout &lay) {
+  lay.big = 0u;
+  lay.threads = std::min<uint32_t>(lay.threads, (uint32_t)TACOS_V4_THREADS);
 }
 
 bool add_lockstep(Layout &lay, uint32_t N, uint32_t L, uint32_t pos_cap, size_t smem_limit) {

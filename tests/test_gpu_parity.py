@@ -582,3 +582,20 @@ def test_topology_first_use_on_side_streams(T):
         assert outs[0] == outs[1] == syn.sends.tobytes()
         del t
     torch.cuda.synchronize()
+
+
+def test_big_thread_bound_kernel(T, monkeypatch):
+    """512 NPUs on one SM (TACOS_CLUSTER=1), one lane and four vectors per destination: the
+    register-path kernel with the 512-thread bound (one destination per walker), on the paper's
+    Ring(2) x FC(4) x Switch(64) system (several link costs, per-event loop) and the 3-D torus;
+    the oracle's schedules, and the same bytes with the default bound (TACOS_NO_BIG=1)."""
+    monkeypatch.setenv("TACOS_CLUSTER", "1")
+    for topo in (W.ring_fc_switch(2, 4, 64, 200, 100, 50), W.torus([8, 8, 8])):
+        syn, sch, t = run_both(T, topo, 1, 1 << 20, "AR", 2)
+        assert_parity(syn, sch, "AR")
+        assert T.Plan(t, "AR", 1, 1 << 20, 2).info()["threads"] == 512
+        monkeypatch.setenv("TACOS_NO_BIG", "1")
+        assert T.Plan(t, "AR", 1, 1 << 20, 2).info()["threads"] <= 384
+        b = T.synthesize(t, "AR", 1, 1 << 20, 2, keep_seed_times=True)
+        assert b.sends.tobytes() == sch.sends.tobytes() and b.result == sch.result
+        monkeypatch.delenv("TACOS_NO_BIG")
